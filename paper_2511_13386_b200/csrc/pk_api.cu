@@ -1,0 +1,436 @@
+// libpk C ABI: context, workspace, pairwise-sum plans and the entry points
+// declared in include/pk.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pk.h"
+#include "pk_args.h"
+
+namespace pk {
+cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st);
+cudaError_t launch_lift(const LiftArgs& a, cudaStream_t st);
+cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
+cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st);
+cudaError_t launch_jump(int64_t n, const double* a, const double* b, double* out, Status* st,
+                        cudaStream_t s);
+cudaError_t launch_maxdiff(int64_t n, const double* a, const double* b, double* err, Status* st,
+                           cudaStream_t s);
+size_t chain_smem_bytes(int nx);
+}  // namespace pk
+
+using pk::PwPlan;
+
+struct pk_ctx {
+  int device = 0;
+  int num_sms = 148;
+  pk::MeshDev m{};
+  double* d_const = nullptr;  // vx | M | xiM | w2
+  PwPlan* d_plan = nullptr;
+  pk::Status* d_status = nullptr;
+  int cap = 0;
+  // workspace
+  double* dws = nullptr;  // 16 double arrays of cap*nx
+  int8_t* i8ws = nullptr;
+  uint8_t* u8ws = nullptr;  // 7 arrays
+  int* iws = nullptr;       // klist cap*nx, nk cap, abort cap
+  std::string err;
+};
+
+namespace {
+
+int fail(pk_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(pk_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, PK_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// numpy pairwise_sum recursion -> leaves + level-ordered internal nodes.
+struct PlanBuilder {
+  std::vector<int> leaf_off, leaf_len;
+  struct Node { int a, b, level; };
+  std::vector<Node> nodes;  // post-order; operands: >=0 leaf, <0 ~node
+  // returns operand id and level
+  std::pair<int, int> rec(int off, int n) {
+    if (n <= 128) {
+      leaf_off.push_back(off);
+      leaf_len.push_back(n);
+      return {(int)leaf_off.size() - 1, 0};
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    auto l = rec(off, n2);
+    auto r = rec(off + n2, n - n2);
+    int lev = std::max(l.second, r.second) + 1;
+    nodes.push_back({l.first, r.first, lev});
+    return {~((int)nodes.size() - 1), lev};
+  }
+};
+
+bool build_plan(int n, PwPlan* P) {
+  PlanBuilder pb;
+  pb.rec(0, n);
+  const int nleaf = (int)pb.leaf_off.size(), nnode = (int)pb.nodes.size();
+  if (nleaf > pk::MAX_LEAF || nnode > pk::MAX_NODE) return false;
+  std::memset(P, 0, sizeof(PwPlan));
+  P->n = n;
+  P->nleaf = nleaf;
+  P->nnode = nnode;
+  for (int i = 0; i < nleaf; ++i) {
+    P->leaf_off[i] = pb.leaf_off[i];
+    P->leaf_len[i] = pb.leaf_len[i];
+  }
+  int maxlev = 0;
+  for (auto& nd : pb.nodes) maxlev = std::max(maxlev, nd.level);
+  if (maxlev > pk::MAX_LEVEL) return false;
+  // stable order by level; map post-order index -> slot
+  std::vector<int> order(nnode), slot(nnode);
+  for (int i = 0; i < nnode; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int x, int y) { return pb.nodes[x].level < pb.nodes[y].level; });
+  for (int i = 0; i < nnode; ++i) slot[order[i]] = i;
+  auto opnd = [&](int id) { return id >= 0 ? id : nleaf + slot[~id]; };
+  for (int i = 0; i < nnode; ++i) {
+    const auto& nd = pb.nodes[order[i]];
+    P->node_a[i] = opnd(nd.a);
+    P->node_b[i] = opnd(nd.b);
+  }
+  P->nlevel = maxlev;
+  for (int lev = 1; lev <= maxlev; ++lev) {
+    int end = 0;
+    for (int i = 0; i < nnode; ++i)
+      if (pb.nodes[order[i]].level <= lev) end = i + 1;
+    P->level_end[lev - 1] = end;
+  }
+  return true;
+}
+
+constexpr int NDWS = 16;
+constexpr int NU8 = 7;
+
+void free_ws(pk_ctx* c) {
+  cudaFree(c->dws);
+  cudaFree(c->i8ws);
+  cudaFree(c->u8ws);
+  cudaFree(c->iws);
+  c->dws = nullptr;
+  c->i8ws = nullptr;
+  c->u8ws = nullptr;
+  c->iws = nullptr;
+  c->cap = 0;
+}
+
+int ensure(pk_ctx* c, int B) {
+  if (B <= c->cap) return PK_OK;
+  cudaSetDevice(c->device);
+  free_ws(c);
+  const size_t n = (size_t)B * c->m.nx;
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->dws, NDWS * n * sizeof(double))) != cudaSuccess) return cuda_fail(c, e, "workspace");
+  if ((e = cudaMalloc(&c->i8ws, n)) != cudaSuccess) return cuda_fail(c, e, "workspace");
+  if ((e = cudaMalloc(&c->u8ws, NU8 * n)) != cudaSuccess) return cuda_fail(c, e, "workspace");
+  if ((e = cudaMalloc(&c->iws, (n + 2 * (size_t)B) * sizeof(int))) != cudaSuccess)
+    return cuda_fail(c, e, "workspace");
+  c->cap = B;
+  return PK_OK;
+}
+
+void bind_ws(pk_ctx* c, pk::FineArgs& a) {
+  const size_t n = (size_t)c->cap * c->m.nx;
+  double* d = c->dws;
+  double** dst[NDWS] = {&a.J, &a.fl, &a.sq, &a.bm, &a.dco, &a.vco, &a.tA, &a.tB,
+                        &a.tC, &a.tD, &a.tE, &a.blift, nullptr, nullptr, nullptr, nullptr};
+  for (int i = 0; i < NDWS; ++i)
+    if (dst[i]) *dst[i] = d + i * n;
+  a.vsg = c->i8ws;
+  uint8_t* u = c->u8ws;
+  a.flip = u;
+  a.nza = u + n;
+  a.nzb = u + 2 * n;
+  a.kcn = u + 3 * n;
+  a.kin = u + 4 * n;
+  a.klist = c->iws;
+  a.nk = c->iws + n;
+  a.abort_ = c->iws + n + c->cap;
+  a.status = c->d_status;
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int32_t pk_version(void) { return 1; }
+
+pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
+  if (!mesh || mesh->nx < 7 || mesh->nv < 1) return nullptr;
+  pk_ctx* c = new pk_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete c;
+    return nullptr;
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  const int nv = mesh->nv, nx = mesh->nx;
+  pk::MeshDev& m = c->m;
+  m.nx = nx;
+  m.nv = nv;
+  m.dx = mesh->dx;
+  m.rdx = 1.0 / mesh->dx;
+  m.two_dx = 2.0 * mesh->dx;
+  m.dvx = mesh->dvx;
+  m.dv3 = mesh->dv3;
+  m.m0 = mesh->m0;
+  m.m2 = mesh->m2;
+  std::memcpy(m.stc, mesh->stencil, sizeof(m.stc));
+  std::memcpy(m.sts, mesh->stencil_scale, sizeof(m.sts));
+  std::vector<double> h(4 * (size_t)nv);
+  std::memcpy(h.data(), mesh->vx, nv * 8);
+  std::memcpy(h.data() + nv, mesh->M, nv * 8);
+  std::memcpy(h.data() + 2 * nv, mesh->xi_M, nv * 8);
+  std::memcpy(h.data() + 3 * nv, mesh->w2, nv * 8);
+  PwPlan plan;
+  if (!build_plan(nx, &plan)) {
+    delete c;
+    return nullptr;
+  }
+  if (cudaMalloc(&c->d_const, h.size() * 8) != cudaSuccess ||
+      cudaMalloc(&c->d_plan, sizeof(PwPlan)) != cudaSuccess ||
+      cudaMalloc(&c->d_status, sizeof(pk::Status)) != cudaSuccess) {
+    delete c;
+    return nullptr;
+  }
+  cudaMemcpy(c->d_const, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(c->d_plan, &plan, sizeof(PwPlan), cudaMemcpyHostToDevice);
+  cudaMemset(c->d_status, 0, sizeof(pk::Status));
+  m.vx = c->d_const;
+  m.M = c->d_const + nv;
+  m.xiM = c->d_const + 2 * nv;
+  m.w2 = c->d_const + 3 * nv;
+  m.plan_x = c->d_plan;
+  return c;
+}
+
+void pk_destroy(pk_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  free_ws(c);
+  cudaFree(c->d_const);
+  cudaFree(c->d_plan);
+  cudaFree(c->d_status);
+  delete c;
+}
+
+const char* pk_last_error(const pk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int32_t pk_reserve(pk_ctx* c, int32_t max_slices) {
+  if (!c || max_slices < 1) return PK_ERR_BAD_ARG;
+  return ensure(c, max_slices);
+}
+
+int32_t pk_status_read(pk_ctx* c, pk_status* out, int32_t clear) {
+  if (!c || !out) return PK_ERR_BAD_ARG;
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(c, e, "synchronize");
+  pk::Status s;
+  e = cudaMemcpy(&s, c->d_status, sizeof(s), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(c, e, "status copy");
+  out->code = s.code;
+  out->slice = s.slice;
+  out->step = s.step;
+  out->pad = 0;
+  if (clear) cudaMemset(c->d_status, 0, sizeof(pk::Status));
+  return PK_OK;
+}
+
+int32_t pk_fine_propagate(pk_ctx* c, int32_t B, double* rho, double* E, double* E_prev,
+                          uint8_t* kc, uint8_t* ki, double* g_a, double* g_b,
+                          const double* rho_bar, const uint8_t* init_flags,
+                          const pk_phase* phases, const pk_hybrid* hyb, double field_rtol,
+                          int32_t cluster_hint, void* stream) {
+  if (!c || B < 1 || !phases || !hyb || !rho || !E || !E_prev || !kc || !ki || !g_a || !g_b ||
+      !rho_bar)
+    return fail(c, PK_ERR_BAD_ARG, "pk_fine_propagate: null argument");
+  const int nv = c->m.nv;
+  if (!(nv == 64 || nv == 128 || nv == 256 || nv == 512 || nv <= 256))
+    return fail(c, PK_ERR_UNSUPPORTED, "pk_fine_propagate: nv not supported");
+  cudaSetDevice(c->device);
+  int r = ensure(c, B);
+  if (r) return r;
+  pk::FineArgs a{};
+  a.m = c->m;
+  a.B = B;
+  a.rho = rho;
+  a.E = E;
+  a.Eprev = E_prev;
+  a.kc = kc;
+  a.ki = ki;
+  a.ga = g_a;
+  a.gb = g_b;
+  a.rho_bar = rho_bar;
+  a.init_flags = init_flags;
+  for (int p = 0; p < 2; ++p) {
+    a.ph[p].nsteps = phases[p].nsteps;
+    a.ph[p].dt = phases[p].dt;
+    a.ph[p].cflu = phases[p].cflu;
+    a.ph[p].k1 = phases[p].kappa1;
+    a.ph[p].k2 = phases[p].kappa2;
+    a.ph[p].cmac = phases[p].cmac;
+    if (!a.ph[p].nsteps || !a.ph[p].dt || !a.ph[p].cflu || !a.ph[p].k1 || !a.ph[p].k2 ||
+        !a.ph[p].cmac)
+      return fail(c, PK_ERR_BAD_ARG, "pk_fine_propagate: incomplete phase");
+  }
+  a.adaptation = hyb->adaptation;
+  a.combine_and = hyb->combine_and;
+  a.reinit = hyb->reinit;
+  a.lift_order = hyb->lift_order;
+  a.time_elim = hyb->time_elim;
+  a.exact_scan = hyb->exact_scan;
+  a.delta0 = hyb->delta0;
+  a.eta0 = hyb->eta0;
+  a.rscale = hyb->rscale;
+  a.neg_eps = hyb->neg_eps;
+  a.eps2 = hyb->eps2;
+  a.rtol = field_rtol;
+  bind_ws(c, a);
+  // cluster size: enough CTAs to fill the chip, >= 4 rows per warp
+  int C = cluster_hint;
+  if (C <= 0) {
+    C = 1;
+    const int slots = 2 * c->num_sms;
+    while (C < 8 && B * C * 2 <= slots && c->m.nx >= (C * 2) * 8 * 4) C *= 2;
+  }
+  a.nwarp_total = C * 8;
+  cudaError_t e = pk::launch_fine(a, C, S(stream));
+  while (e != cudaSuccess && C > 1) {  // cluster too large for this device: shrink
+    cudaGetLastError();
+    C /= 2;
+    a.nwarp_total = C * 8;
+    e = pk::launch_fine(a, C, S(stream));
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "fine launch");
+  return PK_OK;
+}
+
+int32_t pk_coarse_chain(pk_ctx* c, int32_t nchain, int32_t nwin, const double* rho_in,
+                        const double* E_in, double* out, double* gout, double* E_out, const double* delta,
+                        const int32_t* nfull, const double* rem, const double* cflu_full,
+                        const double* cflu_rem, double dt_full, const double* rho_bar,
+                        double field_rtol, int32_t exact_scan, void* stream) {
+  if (!c || nchain < 1 || nwin < 1 || !rho_in || !out || !nfull || !rem || !cflu_full ||
+      !cflu_rem || !rho_bar)
+    return fail(c, PK_ERR_BAD_ARG, "pk_coarse_chain: bad argument");
+  if (pk::chain_smem_bytes(c->m.nx) > 227 * 1024)
+    return fail(c, PK_ERR_UNSUPPORTED, "pk_coarse_chain: nx too large for on-chip state");
+  cudaSetDevice(c->device);
+  pk::ChainArgs a{};
+  a.m = c->m;
+  a.nchain = nchain;
+  a.nwin = nwin;
+  a.rho_in = rho_in;
+  a.E_in = E_in;
+  a.out = out;
+  a.gout = gout;
+  a.Eout = E_out;
+  a.delta = delta;
+  a.nfull = nfull;
+  a.rem = rem;
+  a.cflu_full = cflu_full;
+  a.cflu_rem = cflu_rem;
+  a.dt_full = dt_full;
+  a.rho_bar = rho_bar;
+  a.rtol = field_rtol;
+  a.exact_scan = exact_scan;
+  a.status = c->d_status;
+  cudaError_t e = pk::launch_chain(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "chain launch");
+  return PK_OK;
+}
+
+int32_t pk_field(pk_ctx* c, int32_t B, const double* rho, const double* rho_bar, double* E,
+                 double field_rtol, int32_t exact_scan, void* stream) {
+  if (!c || B < 1 || !rho || !rho_bar || !E) return fail(c, PK_ERR_BAD_ARG, "pk_field: bad argument");
+  cudaSetDevice(c->device);
+  int r = ensure(c, B);
+  if (r) return r;
+  pk::FineArgs w{};
+  bind_ws(c, w);
+  pk::FieldArgs a{};
+  a.m = c->m;
+  a.B = B;
+  a.exact_scan = exact_scan;
+  a.rho = rho;
+  a.rho_bar = rho_bar;
+  a.E = E;
+  a.src = w.tA;
+  a.rtol = field_rtol;
+  a.status = c->d_status;
+  cudaError_t e = pk::launch_field(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "field launch");
+  return PK_OK;
+}
+
+int32_t pk_lift(pk_ctx* c, int32_t B, const double* rho, const double* E, const double* dE_dt,
+                const double* rho_bar, const double* neg_eps, const double* eps2, int32_t order,
+                int32_t time_elim, int32_t project, double* g_out, void* stream) {
+  if (!c || B < 1 || !rho || !E || !rho_bar || !neg_eps || !eps2 || !g_out)
+    return fail(c, PK_ERR_BAD_ARG, "pk_lift: bad argument");
+  if (order != 1 && order != 2) return fail(c, PK_ERR_BAD_LIFT, "lift order must be 1 or 2");
+  if (order == 2 && time_elim != 0 && time_elim != 1)
+    return fail(c, PK_ERR_BAD_LIFT, "time_elim must be 'leading' or 'higher_order'");
+  cudaSetDevice(c->device);
+  int r = ensure(c, B);
+  if (r) return r;
+  pk::FineArgs w{};
+  bind_ws(c, w);
+  pk::LiftArgs a{};
+  a.m = c->m;
+  a.B = B;
+  a.order = order;
+  a.time_elim = time_elim;
+  a.project = project;
+  a.rho = rho;
+  a.E = E;
+  a.dE_dt = dE_dt;
+  a.rho_bar = rho_bar;
+  a.neg_eps = neg_eps;
+  a.eps2 = eps2;
+  a.g_out = g_out;
+  a.J = w.J;
+  a.tA = w.tA;
+  a.tB = w.tB;
+  a.tC = w.tC;
+  a.tD = w.tD;
+  a.tE = w.tE;
+  cudaError_t e = pk::launch_lift(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "lift launch");
+  return PK_OK;
+}
+
+int32_t pk_jump(pk_ctx* c, int64_t n, const double* a, const double* b, double* out, void* stream) {
+  if (!c || n < 1 || !a || !b || !out) return fail(c, PK_ERR_BAD_ARG, "pk_jump: bad argument");
+  cudaSetDevice(c->device);
+  cudaError_t e = pk::launch_jump(n, a, b, out, c->d_status, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "jump launch");
+  return PK_OK;
+}
+
+int32_t pk_maxdiff(pk_ctx* c, int64_t n, const double* a, const double* b, double* err,
+                   void* stream) {
+  if (!c || n < 1 || !a || !b || !err) return fail(c, PK_ERR_BAD_ARG, "pk_maxdiff: bad argument");
+  cudaSetDevice(c->device);
+  cudaError_t e = pk::launch_maxdiff(n, a, b, err, c->d_status, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "maxdiff launch");
+  return PK_OK;
+}
+
+}  // extern "C"

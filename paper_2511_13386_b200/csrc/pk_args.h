@@ -1,0 +1,115 @@
+// Kernel argument blocks (host <-> device), internal to libpk.
+#pragma once
+
+#include <stdint.h>
+
+#include "pk_device.cuh"
+
+namespace pk {
+
+// Velocity-grid constants uploaded once per context (host numpy values,
+// uploaded verbatim: mesh.py:167,211-235; lifting.py:88).
+struct MeshDev {
+  int nx, nv;
+  double dx, rdx, two_dx, dvx, dv3, m0, m2;
+  double three_rb_unused;
+  const double* vx;    // [nv] velocity centres xi_j
+  const double* M;     // [nv] discrete Maxwellian
+  const double* xiM;   // [nv] xi_j * M_j
+  const double* w2;    // [nv] (xi_j^2 - 1) * M_j
+  double stc[4][7];    // 7-point stencil coefficients, offsets -3..3 (adaptation.py:29-34)
+  double sts[4];       // dx ** (-order)
+  const PwPlan* plan_x;  // pairwise plan for nx-term reductions
+};
+
+// One run of identical steps, per slice.
+struct PhaseDev {
+  const int* nsteps;    // [B]
+  const double* dt;     // [B]
+  const double* cflu;   // [B]   m2 * (dt / dx)            (fluid.py:57)
+  const double* k1;     // [B*nx] exp(-dt/eps_i^2)          (kinetic.py:141-145)
+  const double* k2;     // [B*nx] eps_i * -expm1(-dt/eps_i^2)
+  const double* cmac;   // [B*nx] dt / (eps_i * dx)         (kinetic.py:240)
+};
+
+struct FineArgs {
+  MeshDev m;
+  int B;
+  int nwarp_total;       // warps per slice (cluster CTAs x warps per CTA)
+  // state
+  double* rho;           // [B*nx] in/out
+  double* E;             // [B*nx] out: field at the end (also working E)
+  double* Eprev;         // [B*nx] in/out
+  uint8_t* kc;           // [B*nx] in/out kinetic cells
+  uint8_t* ki;           // [B*nx] in/out kinetic interfaces
+  double* ga;            // [B*nx*nv] in/out (result always lands here)
+  double* gb;            // [B*nx*nv] scratch
+  const double* rho_bar; // [B]
+  const uint8_t* init_flags; // [B] bit0: g := lift(rho, E) at entry (parareal.py:171-178)
+                             //     bit1: E_prev := E at entry (HybridState.initial)
+  // schedule
+  PhaseDev ph[2];
+  // hybrid options (hybrid.py:45-55)
+  int adaptation, combine_and, reinit, lift_order, time_elim, exact_scan;
+  double delta0, eta0, rtol;
+  const double* rscale;  // [B*nx] eps_c^2 for scale_remainder, or null
+  const double* neg_eps; // [B*nx] -eps_i
+  const double* eps2;    // [B*nx] eps_i^2
+  // workspace [B*nx] unless noted
+  double *J, *fl, *sq, *bm, *dco, *vco, *tA, *tB, *tC, *tD, *tE, *blift;
+  int8_t* vsg;
+  uint8_t *flip, *nza, *nzb, *kcn, *kin;
+  int* klist;
+  int* nk;               // [B]
+  int* abort_;           // [B]
+  Status* status;
+};
+
+struct LiftArgs {
+  MeshDev m;
+  int B, order, time_elim, project;
+  const double* rho;      // [B*nx]
+  const double* E;        // [B*nx]
+  const double* dE_dt;    // [B*nx] or null
+  const double* rho_bar;  // [B]
+  const double* neg_eps;  // [B*nx]
+  const double* eps2;     // [B*nx]
+  double* g_out;          // [B*nx*nv]
+  double *J, *tA, *tB, *tC, *tD, *tE;  // workspace [B*nx]
+};
+
+struct FieldArgs {
+  MeshDev m;
+  int B, exact_scan;
+  const double* rho;
+  const double* rho_bar;
+  double* E;
+  double* src;            // workspace [B*nx]
+  double rtol;
+  Status* status;
+};
+
+// Coarse drift-diffusion chains (fluid.py:95-118; parareal.py:210-229,276-281).
+// Chain c runs windows w = 0..W-1: in = (w == 0 ? rho_in[c] : out[c][w-1]);
+// G[c][w] = G(in); out[c][w] = G[c][w] (+ delta[c][w] when delta != null).
+struct ChainArgs {
+  MeshDev m;
+  int nchain, nwin;
+  const double* rho_in;  // [nchain*nx]
+  const double* E_in;    // [nchain*nx] field of rho_in for window 0, or null (recompute)
+  double* gout;          // [nchain*nwin*nx] pure G results (may be null)
+  double* out;           // [nchain*nwin*nx]
+  double* Eout;          // [nchain*nx] field after the last window (may be null)
+  const double* delta;   // [nchain*nwin*nx] or null
+  const int* nfull;      // [nchain*nwin]
+  const double* rem;     // [nchain*nwin] clipped last step (0: none)
+  const double* cflu_full;  // [nchain*nwin]
+  const double* cflu_rem;   // [nchain*nwin]
+  double dt_full;           // FluidStepParams.dt (stability checked on the host)
+  const double* rho_bar;    // [nchain]
+  double rtol;
+  int exact_scan;
+  Status* status;
+};
+
+}  // namespace pk

@@ -1,0 +1,171 @@
+// Device helpers shared by the fine-propagator, coarse-propagator and lift
+// kernels.  Compiled with --fmad=false: every multiply and add below rounds
+// separately, exactly like numpy; fused multiply-adds appear only where they
+// are written out explicitly (__fma_rn in qdiv).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pk {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int MAX_LEAF = 160;   // pairwise leaves of <= 128 terms: nx <= 20480
+constexpr int MAX_NODE = 160;
+constexpr int MAX_LEVEL = 10;
+
+// Correctly rounded x / d from rd = RN(1/d): one Markstein correction step.
+// Checked against IEEE division on 3e8 random operands per mesh spacing
+// (tests/test_native_host.py builds the CPU check; tests/test_gpu_parity.py
+// repeats it on the device).  Used for `out /= dx` (kinetic.py:173).
+__device__ __forceinline__ double qdiv(double x, double d, double rd) {
+#ifdef PK_TRUE_DIV
+  return x / d;
+#else
+  double q = x * rd;
+  double r = __fma_rn(-q, d, x);
+  return __fma_rn(r, rd, q);
+#endif
+}
+
+// numpy pairwise-summation plan for an n-term reduction (numpy's
+// pairwise_sum: <8 sequential, <=128 eight accumulators, else split at
+// n/2 rounded down to a multiple of 8).  Leaves in order, internal nodes
+// bottom-up by level; built on the host (pk_api.cu) per n.
+struct PwPlan {
+  int n, nleaf, nnode, nlevel;
+  int leaf_off[MAX_LEAF];
+  int leaf_len[MAX_LEAF];
+  int node_a[MAX_NODE];      // operand indices into vals[nleaf + nnode]
+  int node_b[MAX_NODE];
+  int level_end[MAX_LEVEL];  // nodes [level_end[l-1], level_end[l]) form level l
+};
+
+// One pairwise leaf (n <= 128) over x[off .. off+n) computed by a whole warp;
+// every lane returns the same bits.  Lanes 8..31 duplicate lanes 0..7's
+// accumulators so the butterfly stays within groups of eight.
+template <class F>
+__device__ __forceinline__ double warp_leaf(F x, int off, int n, int lane) {
+  if (n < 8) {
+    double r = -0.0;
+    for (int i = 0; i < n; ++i) r = r + x(off + i);
+    return r;
+  }
+  const int k = lane & 7;
+  const int full = n - (n % 8);
+  double r = x(off + k);
+  for (int i = 8; i < full; i += 8) r = r + x(off + i + k);
+  r = r + __shfl_xor_sync(FULL, r, 1);
+  r = r + __shfl_xor_sync(FULL, r, 2);
+  r = r + __shfl_xor_sync(FULL, r, 4);
+  for (int i = full; i < n; ++i) r = r + x(off + i);
+  return r;
+}
+
+// Block-wide pairwise sum following a plan.  `scratch` is shared memory of at
+// least nleaf + nnode doubles.  Every thread of the block must call it; every
+// thread gets the result.
+template <class F>
+__device__ double block_pairwise(F x, const PwPlan& P, double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarp = blockDim.x >> 5;
+  for (int l = warp; l < P.nleaf; l += nwarp) {
+    double v = warp_leaf(x, P.leaf_off[l], P.leaf_len[l], lane);
+    if (lane == 0) scratch[l] = v;
+  }
+  __syncthreads();
+  int start = 0;
+  for (int lev = 0; lev < P.nlevel; ++lev) {
+    const int end = P.level_end[lev];
+    for (int j = start + threadIdx.x; j < end; j += blockDim.x)
+      scratch[P.nleaf + j] = scratch[P.node_a[j]] + scratch[P.node_b[j]];
+    __syncthreads();
+    start = end;
+  }
+  // root: the single leaf, or the last internal node
+  const double res = scratch[P.nnode == 0 ? 0 : P.nleaf + P.nnode - 1];
+  __syncthreads();
+  return res;
+}
+
+// Sequential prefix sum (np.cumsum order) of src into dst by warp 0 of the
+// block; values are staged 32 at a time and shuffled to every lane so the
+// only serial dependency is the add chain.  Other warps return immediately.
+template <class FS, class FD>
+__device__ __forceinline__ void warp_cumsum(FS src, FD dst, int n) {
+  if ((threadIdx.x >> 5) != 0) return;
+  const int lane = threadIdx.x & 31;
+  double acc = -0.0;  // -0.0 + t == t bitwise: out[0] = src[0]
+  for (int base = 0; base < n; base += 32) {
+    const int m = min(32, n - base);
+    const double v = (lane < m) ? src(base + lane) : 0.0;
+    double mine = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      if (j < m) {
+        const double t = __shfl_sync(FULL, v, j);
+        acc = acc + t;
+        if (lane == j) mine = acc;
+      }
+    }
+    if (lane < m) dst(base + lane, mine);
+  }
+}
+
+// Work-efficient parallel prefix sum (fast mode, not bitwise): block scan with
+// warp shuffles over a blocked partition.  `scratch` holds blockDim.x/32 + 1
+// doubles.  Result differs from np.cumsum by O(n u |E|).
+template <class FS, class FD>
+__device__ void block_scan_fast(FS src, FD dst, int n, double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarp = blockDim.x >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, threadIdx.x * per), hi = min(n, lo + per);
+  double s = 0.0;
+  for (int i = lo; i < hi; ++i) s = s + src(i);
+  double inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double t = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc = inc + t;
+  }
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    double w = (lane < nwarp) ? scratch[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      double t = __shfl_up_sync(FULL, w, o);
+      if (lane >= o) w = w + t;
+    }
+    if (lane < nwarp) scratch[lane] = w;
+  }
+  __syncthreads();
+  double run = (inc - s) + (warp > 0 ? scratch[warp - 1] : 0.0);
+  for (int i = lo; i < hi; ++i) {
+    run = run + src(i);
+    dst(i, run);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int wrap(int i, int n) {
+  return i < 0 ? i + n : (i >= n ? i - n : i);
+}
+
+// Status record: first error wins.
+struct Status {
+  int code;   // pk.h PK_ERR_*
+  int slice;
+  int step;
+  int pad;
+};
+
+__device__ __forceinline__ void set_status(Status* st, int code, int slice, int step) {
+  if (atomicCAS(&st->code, 0, code) == 0) {
+    st->slice = slice;
+    st->step = step;
+  }
+}
+
+}  // namespace pk

@@ -1,0 +1,171 @@
+// Coarse propagator G (explicit drift-diffusion limit scheme) and the small
+// parareal glue kernels.
+//
+// One CTA owns one chain of windows and keeps rho, E and J in shared memory
+// for the whole chain: the per-step work is O(nx) and strictly sequential in
+// time (fluid.py:60-118), so the kernel is latency-bound; keeping the state
+// on-chip removes every global round trip from the step loop.
+#include "../../include/pk.h"
+#include "pk_args.h"
+
+namespace pk {
+
+__device__ static bool chain_field(const MeshDev& m, const double* rho, double rb, double* src,
+                                   double* E, double rtol, int exact_scan, const PwPlan& plan,
+                                   double* red) {
+  const int nx = m.nx;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = (rho[i] - rb) * m.dx;
+  __syncthreads();
+  const double defect = block_pairwise([&](int i) { return src[i]; }, plan, red);
+  const double scale = block_pairwise([&](int i) { return fabs(rho[i]); }, plan, red) * m.dx;
+  if (fabs(defect) > rtol * fmax(scale, 2.2250738585072014e-308)) return false;
+  const double corr = defect / (double)nx;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = src[i] - corr;
+  __syncthreads();
+  if (exact_scan) {
+    warp_cumsum([&](int i) { return src[i]; }, [&](int i, double v) { E[i] = v; }, nx);
+  } else {
+    block_scan_fast([&](int i) { return src[i]; }, [&](int i, double v) { E[i] = v; }, nx, red);
+  }
+  __syncthreads();
+  const double mean = block_pairwise([&](int i) { return E[i]; }, plan, red) / (double)nx;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) E[i] = E[i] - mean;
+  __syncthreads();
+  return true;
+}
+
+__global__ void __launch_bounds__(512) chain_kernel(const ChainArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const MeshDev& m = a.m;
+  const int nx = m.nx;
+  const int c = blockIdx.x;
+  PwPlan* plan = reinterpret_cast<PwPlan*>(smem_raw);
+  double* base = reinterpret_cast<double*>(smem_raw + (sizeof(PwPlan) + 15) / 16 * 16);
+  double* rho = base;
+  double* E = rho + nx;
+  double* J = E + nx;
+  double* src = J + nx;
+  double* red = src + nx;
+  {
+    const int* s = reinterpret_cast<const int*>(m.plan_x);
+    int* d = reinterpret_cast<int*>(plan);
+    for (int i = threadIdx.x; i < (int)(sizeof(PwPlan) / 4); i += blockDim.x) d[i] = s[i];
+  }
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) rho[i] = a.rho_in[(size_t)c * nx + i];
+  __syncthreads();
+  const double rb = a.rho_bar[c];
+  bool have_E = false;
+  for (int w = 0; w < a.nwin; ++w) {
+    const size_t cw = (size_t)c * a.nwin + w;
+    const int nfull = a.nfull[cw];
+    const double rem = a.rem[cw];
+    if (nfull > 0 || rem > 0.0) {
+      if (w == 0 && a.E_in) {
+        // fluid_step: the caller guarantees E matches rho (fluid.py:69-71)
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) E[i] = a.E_in[(size_t)c * nx + i];
+        __syncthreads();
+      } else if (!chain_field(m, rho, rb, src, E, a.rtol, a.exact_scan, *plan, red)) {
+        // fluid_propagate: the field is refreshed from rho on entry (fluid.py:111-113)
+        if (threadIdx.x == 0) set_status(a.status, PK_ERR_SOLVABILITY, c, w);
+        return;
+      }
+      have_E = true;
+      const int nstep = nfull + (rem > 0.0 ? 1 : 0);
+      for (int s = 0; s < nstep; ++s) {
+        const double cflu = s < nfull ? a.cflu_full[cw] : a.cflu_rem[cw];
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+          const int in_ = i + 1 == nx ? 0 : i + 1;
+          const double r = rho[i], rn = rho[in_];
+          J[i] = (rn - r) / m.dx - E[i] * 0.5 * (r + rn);   // fluid.py:51-52
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+          const int ip = i == 0 ? nx - 1 : i - 1;
+          rho[i] = rho[i] + cflu * (J[i] - J[ip]);           // fluid.py:57
+        }
+        __syncthreads();
+        if (!chain_field(m, rho, rb, src, E, a.rtol, a.exact_scan, *plan, red)) {
+          if (threadIdx.x == 0) set_status(a.status, PK_ERR_SOLVABILITY, c, w);
+          return;
+        }
+      }
+    }
+    if (a.gout)
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) a.gout[cw * nx + i] = rho[i];
+    if (a.delta) {
+      // new_row[n] = coarse.rho + deltas[n]   (parareal.py:281)
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) rho[i] = rho[i] + a.delta[cw * nx + i];
+    }
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) a.out[cw * nx + i] = rho[i];
+    __syncthreads();
+  }
+  if (a.Eout && have_E)
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) a.Eout[(size_t)c * nx + i] = E[i];
+}
+
+size_t chain_smem_bytes(int nx) {
+  return (sizeof(PwPlan) + 15) / 16 * 16 + (size_t)4 * nx * 8 + (MAX_LEAF + MAX_NODE) * 8;
+}
+
+cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st) {
+  const size_t smem = chain_smem_bytes(a.m.nx);
+  cudaError_t e =
+      cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  chain_kernel<<<a.nchain, 512, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Delta = F - G (parareal.py:429) and the finiteness check of parareal.py:267-269.
+__global__ void jump_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                            double* __restrict__ out, Status* st) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = a[i] - b[i];
+    out[i] = d;
+    bad |= !isfinite(d);
+  }
+  if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) set_status(st, PK_ERR_NONFINITE, -1, -1);
+}
+
+cudaError_t launch_jump(int64_t n, const double* a, const double* b, double* out, Status* st,
+                        cudaStream_t s) {
+  const int64_t want = (n + 255) / 256;
+  const int blocks = (int)(want < 148 * 4 ? want : 148 * 4);
+  jump_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(n, a, b, out, st);
+  return cudaGetLastError();
+}
+
+// err = max |a - b| (parareal.py:286); max is order-independent, so a tree is
+// exact.  Also flags a non-finite a (parareal.py:283-284).  One CTA.
+__global__ void maxdiff_kernel(int64_t n, const double* __restrict__ a,
+                               const double* __restrict__ b, double* err, Status* st) {
+  __shared__ double sm[32];
+  double mx = 0.0;
+  bool bad = false;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = fabs(a[i] - b[i]);
+    bad |= !isfinite(a[i]);
+    mx = fmax(mx, d);  // numpy max propagates NaN; non-finite already raises
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) set_status(st, PK_ERR_NONFINITE, -1, -1);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+    if (threadIdx.x == 0) *err = v;
+  }
+}
+
+cudaError_t launch_maxdiff(int64_t n, const double* a, const double* b, double* err, Status* st,
+                           cudaStream_t s) {
+  maxdiff_kernel<<<1, 1024, 0, s>>>(n, a, b, err, st);
+  return cudaGetLastError();
+}
+
+}  // namespace pk

@@ -1,0 +1,324 @@
+"""Device engine: one libpk context per (CUDA device, mesh), batched entry
+points on torch CUDA tensors, and the host-side formation of the scalar
+constants the kernels consume.
+
+Everything numeric that the reference forms as a Python float (kappa1/2,
+dt/(eps dx), m2 (dt/dx), eps**2, dx**-p, ...) is formed here the same way and
+uploaded, so the device arithmetic starts from bit-identical constants
+(SURVEY F10).  torch is used only for device memory and streams.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import NativeError, raise_for
+from .mesh import PhaseMesh
+
+STENCIL_COEFFS = {  # adaptation.py:29-34 (Python floats)
+    1: (-1 / 60, 3 / 20, -3 / 4, 0.0, 3 / 4, -3 / 20, 1 / 60),
+    2: (1 / 90, -3 / 20, 3 / 2, -49 / 18, 3 / 2, -3 / 20, 1 / 90),
+    3: (1 / 8, -1.0, 13 / 8, 0.0, -13 / 8, 1.0, -1 / 8),
+    4: (-1 / 6, 2.0, -13 / 2, 28 / 3, -13 / 2, 2.0, -1 / 6),
+}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def relaxation_coefficients(dt: float, eps: float):
+    """(e^{-dt/eps^2}, eps (1 - e^{-dt/eps^2})) (kinetic.py:141-145)."""
+    z = dt / eps**2
+    return float(np.exp(-z)), float(eps * (-np.expm1(-z)))
+
+
+@dataclass
+class Phase:
+    """Host description of one run of identical steps for B slices."""
+
+    nsteps: np.ndarray   # int32 [B]
+    dt: np.ndarray       # [B]
+    cflu: np.ndarray     # [B]
+    k1: np.ndarray       # [B, nx]
+    k2: np.ndarray       # [B, nx]
+    cmac: np.ndarray     # [B, nx]
+
+
+def eps_rows(eps, nx: int) -> np.ndarray:
+    """Per-interface eps values of a scalar or an EpsProfile."""
+    iface = getattr(eps, "iface", None)
+    if iface is not None:
+        return np.asarray(iface, dtype=float)
+    return np.full(nx, float(eps))
+
+
+def eps_cells(eps, nx: int) -> np.ndarray:
+    cell = getattr(eps, "cell", None)
+    if cell is not None:
+        return np.asarray(cell, dtype=float)
+    return np.full(nx, float(eps))
+
+
+def per_value(values: np.ndarray, fn) -> np.ndarray:
+    """Apply a scalar Python-float rule once per distinct value."""
+    out = np.empty(values.shape[0])
+    cache = {}
+    for i, e in enumerate(values.tolist()):
+        r = cache.get(e)
+        if r is None:
+            r = cache[e] = fn(e)
+        out[i] = r
+    return out
+
+
+def make_phase(mesh: PhaseMesh, eps_list, dt_list, nsteps_list) -> Phase:
+    """Coefficients of a run of steps; slice b uses eps_list[b], dt_list[b]."""
+    B = len(eps_list)
+    nx, dx, m2 = mesh.nx, mesh.dx, mesh.vgrid.m2
+    k1 = np.empty((B, nx))
+    k2 = np.empty((B, nx))
+    cm = np.empty((B, nx))
+    cflu = np.empty(B)
+    dts = np.empty(B)
+    for b in range(B):
+        dt = float(dt_list[b])
+        dts[b] = dt
+        e = eps_rows(eps_list[b], nx)
+        k1[b] = per_value(e, lambda v: relaxation_coefficients(dt, v)[0])
+        k2[b] = per_value(e, lambda v: relaxation_coefficients(dt, v)[1])
+        cm[b] = per_value(e, lambda v: dt / (v * dx))
+        cflu[b] = m2 * (dt / dx)
+    return Phase(np.asarray(nsteps_list, dtype=np.int32), dts, cflu, k1, k2, cm)
+
+
+@dataclass
+class HybridKnobs:
+    adaptation: bool = False
+    combine: str = "or"
+    scale_remainder: bool = False
+    reinit: str = "lift"
+    lift_order: int = 2
+    time_elim: str = "leading"
+    delta0: float = 1.0
+    eta0: float = 1.0
+
+
+def _combine_code(c):
+    if c == "or":
+        return 0
+    if c == "and":
+        return 1
+    raise ValueError(f"combine must be 'or' or 'and', got {c!r}")
+
+
+class Device:
+    """libpk context bound to one mesh on one CUDA device."""
+
+    _cache: dict = {}
+    _lock = threading.Lock()
+
+    @classmethod
+    def for_mesh(cls, mesh: PhaseMesh, device=None) -> "Device":
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise NativeError("no CUDA device: the B200 engine has no CPU fallback")
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                           torch.device(device).index or 0)
+        key = (dev.index, id(mesh))
+        with cls._lock:
+            d = cls._cache.get(key)
+            if d is None or d.mesh is not mesh:
+                d = cls._cache[key] = cls(mesh, dev)
+            return d
+
+    def __init__(self, mesh: PhaseMesh, device):
+        torch = _torch()
+        self.lib = _native.load()
+        self.mesh = mesh
+        self.device = torch.device(device)
+        self.nx = mesh.nx
+        self.nv = mesh.nv
+        grid = mesh.vgrid
+        vx = np.ascontiguousarray(grid.vx, dtype=float)
+        M = np.ascontiguousarray(grid.M.reshape(-1))
+        xiM = np.ascontiguousarray(mesh.xi_M.reshape(-1))
+        w2 = np.ascontiguousarray(((grid.xi**2 - 1.0) * grid.M).reshape(-1))
+        self._keep = (vx, M, xiM, w2)
+        m = _native.PkMesh()
+        m.nx, m.nv = mesh.nx, self.nv
+        m.dx, m.dvx, m.dv3 = mesh.dx, grid.dvx, grid.dv3
+        m.m0, m.m2, m.x_star, m.v_star = grid.m0, grid.m2, mesh.x_star, mesh.v_star
+        dp = lambda a: a.ctypes.data_as(_native.c_double_p)  # noqa: E731
+        m.vx, m.M, m.xi_M, m.w2 = dp(vx), dp(M), dp(xiM), dp(w2)
+        for p in range(4):
+            for o in range(7):
+                m.stencil[p][o] = STENCIL_COEFFS[p + 1][o]
+            m.stencil_scale[p] = mesh.dx ** (-(p + 1))
+        with torch.cuda.device(self.device):
+            torch.cuda.init()
+            self.ctx = self.lib.pk_create(self.device.index or 0, C.byref(m))
+        if not self.ctx:
+            raise NativeError("pk_create failed (unsupported mesh or CUDA error)")
+        self._scratch = {}
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx:
+            try:
+                self.lib.pk_destroy(ctx)
+            except Exception:
+                pass
+
+    # -- helpers -------------------------------------------------------------
+    @property
+    def stream(self):
+        torch = _torch()
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def t(self, a, dtype=None):
+        """Host array -> contiguous device tensor."""
+        torch = _torch()
+        if isinstance(a, torch.Tensor):
+            return a.to(device=self.device, dtype=dtype or a.dtype).contiguous()
+        a = np.ascontiguousarray(a)
+        return torch.from_numpy(a).to(self.device, non_blocking=False)
+
+    def scratch(self, name, shape, dtype=None):
+        torch = _torch()
+        dtype = dtype or torch.float64
+        key = (name, tuple(shape), dtype)
+        buf = self._scratch.get(key)
+        if buf is None:
+            buf = self._scratch[key] = torch.empty(shape, dtype=dtype, device=self.device)
+        return buf
+
+    def _rc(self, code, what):
+        if code != 0:
+            msg = self.lib.pk_last_error(self.ctx)
+            raise_for(code, f"{what}: {msg.decode() if msg else ''}")
+
+    def check(self):
+        """Synchronise and raise the latched device status, if any."""
+        st = _native.PkStatus()
+        self._rc(self.lib.pk_status_read(self.ctx, C.byref(st), 1), "status")
+        if st.code:
+            raise_for(st.code, f"slice {st.slice}, step {st.step}")
+
+    def reserve(self, B):
+        self._rc(self.lib.pk_reserve(self.ctx, int(B)), "reserve")
+
+    # -- entry points --------------------------------------------------------
+    def phase_dev(self, ph: Phase):
+        torch = _torch()
+        dev = dict(
+            nsteps=self.t(ph.nsteps.astype(np.int32)), dt=self.t(ph.dt), cflu=self.t(ph.cflu),
+            k1=self.t(ph.k1), k2=self.t(ph.k2), cmac=self.t(ph.cmac))
+        s = _native.PkPhase()
+        s.nsteps, s.dt, s.cflu = _ptr(dev["nsteps"]), _ptr(dev["dt"]), _ptr(dev["cflu"])
+        s.kappa1, s.kappa2, s.cmac = _ptr(dev["k1"]), _ptr(dev["k2"]), _ptr(dev["cmac"])
+        del torch
+        return s, dev
+
+    def fine(self, rho, E, Eprev, kc, ki, g, rho_bar, init_flags, phases, knobs: HybridKnobs,
+             eps_list, rtol, exact_scan=True, cluster_hint=0, prepared=None):
+        """Advance B slices in place (device tensors).  ``phases``: [full, rem]."""
+        B = rho.shape[0]
+        nx, nv = self.nx, self.nv
+        if prepared is None:
+            prepared = self.prepare_fine(B, phases, knobs, eps_list)
+        ph_structs, hyb, keep = prepared
+        gb = self.scratch("gb", (B, nx, nv))
+        self.reserve(B)
+        flags = self.t(np.asarray(init_flags, dtype=np.uint8))
+        rc = self.lib.pk_fine_propagate(
+            self.ctx, B, _ptr(rho), _ptr(E), _ptr(Eprev), _ptr(kc), _ptr(ki), _ptr(g), _ptr(gb),
+            _ptr(rho_bar), _ptr(flags), ph_structs, C.byref(hyb), float(rtol),
+            int(cluster_hint), self.stream)
+        self._rc(rc, "pk_fine_propagate")
+        self._keepalive = (keep, flags)
+
+    def prepare_fine(self, B, phases, knobs: HybridKnobs, eps_list):
+        """Upload phase coefficients and hybrid knobs (reusable across calls)."""
+        nx = self.nx
+        arr = (_native.PkPhase * 2)()
+        keep = []
+        for p in range(2):
+            s, dev = self.phase_dev(phases[p])
+            arr[p] = s
+            keep.append(dev)
+        hyb = _native.PkHybrid()
+        hyb.adaptation = int(bool(knobs.adaptation))
+        hyb.combine_and = _combine_code(knobs.combine) if knobs.adaptation else 0
+        hyb.reinit = {"lift": 0, "zero": 1}.get(knobs.reinit, 2)
+        hyb.lift_order = int(knobs.lift_order) if knobs.lift_order in (1, 2) else 0
+        hyb.time_elim = {"leading": 0, "higher_order": 1}.get(knobs.time_elim, 2)
+        hyb.exact_scan = 1
+        hyb.delta0, hyb.eta0 = float(knobs.delta0), float(knobs.eta0)
+        neg = np.stack([per_value(eps_rows(e, nx), lambda v: -v) for e in eps_list])
+        e2 = np.stack([per_value(eps_rows(e, nx), lambda v: v**2) for e in eps_list])
+        dneg, de2 = self.t(neg), self.t(e2)
+        hyb.neg_eps, hyb.eps2 = _ptr(dneg), _ptr(de2)
+        keep += [dneg, de2]
+        if knobs.adaptation and knobs.scale_remainder:
+            rs = self.t(np.stack([per_value(eps_cells(e, nx), lambda v: v**2) for e in eps_list]))
+            hyb.rscale = _ptr(rs)
+            keep.append(rs)
+        else:
+            hyb.rscale = C.c_void_p(0)
+        return arr, hyb, keep
+
+    def chain(self, rho_in, out, gout, E_out, delta, nfull, rem, dt_full, rho_bar, rtol,
+              exact_scan=True, E_in=None, m2=None):
+        """Coarse chains: rho_in [nchain, nx], out/gout/delta [nchain, nwin, nx]."""
+        nchain, nwin = out.shape[0], out.shape[1]
+        dx = self.mesh.dx
+        m2 = self.mesh.vgrid.m2 if m2 is None else m2
+        nfull = np.asarray(nfull, dtype=np.int32).reshape(nchain, nwin)
+        rem = np.asarray(rem, dtype=float).reshape(nchain, nwin)
+        cf = np.full((nchain, nwin), m2 * (dt_full / dx))
+        cr = np.vectorize(lambda r: m2 * (r / dx) if r > 0.0 else 0.0)(rem) if rem.size else rem
+        d_nf, d_rem, d_cf, d_cr = self.t(nfull), self.t(rem), self.t(cf), self.t(np.asarray(cr, float))
+        rc = self.lib.pk_coarse_chain(
+            self.ctx, nchain, nwin, _ptr(rho_in), _ptr(E_in), _ptr(out), _ptr(gout), _ptr(E_out),
+            _ptr(delta),
+            _ptr(d_nf), _ptr(d_rem), _ptr(d_cf), _ptr(d_cr), float(dt_full), _ptr(rho_bar),
+            float(rtol), int(bool(exact_scan)), self.stream)
+        self._rc(rc, "pk_coarse_chain")
+        self._keepalive = (d_nf, d_rem, d_cf, d_cr)
+
+    def field(self, rho, rho_bar, E, rtol, exact_scan=True):
+        self.reserve(rho.shape[0])
+        rc = self.lib.pk_field(self.ctx, rho.shape[0], _ptr(rho), _ptr(rho_bar), _ptr(E),
+                               float(rtol), int(bool(exact_scan)), self.stream)
+        self._rc(rc, "pk_field")
+
+    def lift(self, rho, E, dE_dt, rho_bar, eps_list, order, time_elim, project, g_out):
+        B, nx = rho.shape
+        self.reserve(B)
+        neg = self.t(np.stack([per_value(eps_rows(e, nx), lambda v: -v) for e in eps_list]))
+        e2 = self.t(np.stack([per_value(eps_rows(e, nx), lambda v: v**2) for e in eps_list]))
+        te = {"leading": 0, "higher_order": 1}.get(time_elim, 2)
+        rc = self.lib.pk_lift(self.ctx, B, _ptr(rho), _ptr(E), _ptr(dE_dt), _ptr(rho_bar),
+                              _ptr(neg), _ptr(e2), int(order), te, int(bool(project)),
+                              _ptr(g_out), self.stream)
+        self._rc(rc, "pk_lift")
+        self._keepalive = (neg, e2)
+
+    def jump(self, a, b, out):
+        rc = self.lib.pk_jump(self.ctx, a.numel(), _ptr(a), _ptr(b), _ptr(out), self.stream)
+        self._rc(rc, "pk_jump")
+
+    def maxdiff(self, a, b, err):
+        rc = self.lib.pk_maxdiff(self.ctx, a.numel(), _ptr(a), _ptr(b), _ptr(err), self.stream)
+        self._rc(rc, "pk_maxdiff")

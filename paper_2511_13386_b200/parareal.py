@@ -1,0 +1,529 @@
+"""Parallel-in-time driver (parareal.py:1-452), device-resident.
+
+Algorithm 1 of the paper with the reference's semantics: coarse sweep, jumps
+Delta^n = F(rho^{n-1,k}) - G(rho^{n-1,k}) for the unconverged windows
+n = k+1..Ng, sequential correction rho^{n,k+1} = G(rho^{n-1,k+1}) + Delta^n,
+successive error max|row_{k+1} - row_k|, stop at err < tol or k_max.
+
+B200 design:
+  * all active windows of an iteration are ONE launch of the persistent fine
+    kernel (one thread-block cluster per window, libpk pk_fine_propagate);
+  * G(rho^{n-1,k}) is taken from the previous correction / the coarse sweep
+    instead of being recomputed (bit-identical);
+  * the correction and the coarse sweep are one launch each (one CTA walks the
+    windows sequentially with rho/E in shared memory, pk_coarse_chain);
+  * multi-GPU: one process per GPU (torch.distributed, NCCL); the active
+    windows are dealt cyclically to ranks, the fine results are all-gathered
+    (the only exchange, (Ng - k) x nx doubles per iteration), and every rank
+    runs the cheap correction redundantly, so the ledgers are bit-identical on
+    all ranks and no broadcast is needed.  Results do not depend on the
+    number of GPUs (cf. tests/test_parareal.py:93-101).
+The host only forms schedules and reads one scalar (err) per iteration.
+
+``_fine_window`` keeps the reference's plugin seam (parareal.py:153-190): if
+it is monkeypatched, ``parareal_iterate`` calls it per window exactly as the
+reference's ``_jump_task`` does.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .adaptation import Thresholds
+from .engine import Device, make_phase
+from .errors import NonFiniteState
+from .fluid import FluidStepParams, fluid_propagate, substep_sizes
+from .hybrid import HybridOptions, HybridState, hybrid_propagate, knobs_of
+from .kinetic import KineticStepParams
+from .lifting import lift
+from .mesh import MacroState, MicroState, PhaseMesh
+from .poisson import SOLVABILITY_RTOL, solve_field
+
+WORKERS_ENV = "PARAKIN_WORKERS"
+ADAPTIVE_FIELD_RTOL = 1e-5
+
+
+def field_guard(cfg: "PararealConfig"):
+    return ADAPTIVE_FIELD_RTOL if cfg.options.adaptation else None
+
+
+@dataclass(frozen=True)
+class PararealConfig:
+    eps: object
+    t_final: float
+    ng: int
+    k_max: int = 50
+    tol: float = 1e-10
+    workers: int = 1
+    parareal_enabled: bool = True
+    thresholds: Thresholds = Thresholds(1e-5, 1e-5)
+    options: HybridOptions = HybridOptions()
+
+    def __post_init__(self):
+        if self.ng < 1:
+            raise ValueError("ng must be >= 1")
+        if self.tol <= 0.0:
+            raise ValueError("tol must be positive")
+
+    @property
+    def boundaries(self) -> np.ndarray:
+        return np.linspace(0.0, self.t_final, self.ng + 1)
+
+
+@dataclass
+class PhaseTimings:
+    coarse_sweep: float = 0.0
+    fine_max: float = 0.0
+    fine_total: float = 0.0
+    lift_max: float = 0.0
+    lift_total: float = 0.0
+    fluid_window_max: float = 0.0
+    correction_total: float = 0.0
+    wall_total: float = 0.0
+    iterations: list = field(default_factory=list)
+
+
+@dataclass
+class PararealLedger:
+    boundaries: np.ndarray
+    rho: list
+    jumps: list = field(default_factory=list)
+    err: list = field(default_factory=list)
+    kinetic_fraction: np.ndarray | None = None
+    timings: PhaseTimings = field(default_factory=PhaseTimings)
+
+    def masses(self, dx: float) -> np.ndarray:
+        return np.stack([row.sum(axis=1) * dx for row in self.rho])
+
+
+@dataclass
+class RunResult:
+    status: str
+    iterations: int
+    ledger: PararealLedger
+    boundary_rho: np.ndarray
+    kinetic_fraction: np.ndarray
+    config: PararealConfig
+
+    def boundary_fields(self, mesh: PhaseMesh, rho_bar: float) -> np.ndarray:
+        rtol = field_guard(self.config)
+        return np.stack([solve_field(r, rho_bar, mesh, rtol=rtol) for r in self.boundary_rho])
+
+
+def resolve_workers(requested: int | None = None) -> int:
+    env = os.environ.get(WORKERS_ENV)
+    if env:
+        return max(1, int(env))
+    if requested is not None and requested > 0:
+        return requested
+    return 1
+
+
+def default_params(cfg: PararealConfig, mesh: PhaseMesh, E0) -> tuple:
+    """parareal.py:138-146."""
+    fluid_p = FluidStepParams.default(mesh)
+    kin_p = KineticStepParams.default(mesh, cfg.eps, e_max=float(np.max(np.abs(E0))))
+    return fluid_p, kin_p
+
+
+# ---------------------------------------------------------------------------
+# communicator (one process per GPU)
+
+
+class _Comm:
+    def __init__(self):
+        self.rank, self.size, self.dist = 0, 1, None
+        try:
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized():
+                self.dist = dist
+                self.rank, self.size = dist.get_rank(), dist.get_world_size()
+        except Exception:
+            pass
+
+    def all_gather(self, t):
+        if self.size == 1:
+            return [t]
+        import torch
+        parts = [torch.empty_like(t) for _ in range(self.size)]
+        self.dist.all_gather(parts, t.contiguous())
+        return parts
+
+
+# ---------------------------------------------------------------------------
+# device engine
+
+
+class _Engine:
+    """Device-resident state of one parareal run."""
+
+    def __init__(self, cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p, comm=None):
+        import torch
+
+        self.torch = torch
+        self.cfg, self.mesh, self.fluid_p, self.kin_p = cfg, mesh, fluid_p, kin_p
+        self.dev = Device.for_mesh(mesh)
+        self.comm = comm or _Comm()
+        self.rho_bar = float(rho_bar)
+        self.nx, self.nv, ng = mesh.nx, mesh.nv, cfg.ng
+        b = cfg.boundaries
+        self.bounds = b
+        self.sc = [substep_sizes(float(b[n - 1]), float(b[n]), fluid_p.dt) for n in range(1, ng + 1)]
+        self.sf = [substep_sizes(float(b[n - 1]), float(b[n]), kin_p.dt) for n in range(1, ng + 1)]
+        for nf, rem in self.sc:
+            if nf:
+                fluid_p.check(fluid_p.dt, mesh)
+            if rem > 0.0:
+                fluid_p.check(rem, mesh)
+        for nf, rem in self.sf:
+            if nf:
+                kin_p.check(kin_p.dt, mesh)
+            if rem > 0.0:
+                kin_p.check(rem, mesh)
+        self.rtol = field_guard(cfg)
+        self.rtol_f = SOLVABILITY_RTOL if self.rtol is None else self.rtol
+        dev = self.dev
+        self.row = dev.t(np.ascontiguousarray(np.repeat(np.asarray(rho0, float)[None], ng + 1, 0)))
+        self.G = torch.empty_like(self.row)    # G[n] = G(row_k[n-1])
+        self.g0 = dev.t(np.ascontiguousarray(np.asarray(g0, float).reshape(self.nx, self.nv)))
+        self.rb1 = dev.t(np.array([self.rho_bar]))
+        self.knobs = knobs_of(cfg.options, cfg.thresholds)
+        self.err_d = torch.zeros(1, dtype=torch.float64, device=dev.device)
+
+    # coarse chain over windows n0..n1 (1-based, inclusive) starting from x
+    def _chain(self, x, n0, n1, out, gout, delta, rtol):
+        sc = self.sc[n0 - 1:n1]
+        self.dev.chain(x.reshape(1, self.nx), out.reshape(1, -1, self.nx),
+                       None if gout is None else gout.reshape(1, -1, self.nx), None,
+                       None if delta is None else delta.reshape(1, -1, self.nx),
+                       [s[0] for s in sc], [s[1] for s in sc], self.fluid_p.dt, self.rb1,
+                       SOLVABILITY_RTOL if rtol is None else rtol, m2=self.fluid_p.m2)
+
+    def coarse_sweep(self):
+        ng = self.cfg.ng
+        self._chain(self.row[0], 1, ng, self.row[1:], None, None, None)
+        self.G[1:] = self.row[1:]   # G(row_0[n-1]) == row_0[n]
+        self.dev.check()
+
+    def fine(self, windows):
+        """F for the given windows (this rank's share); returns (rho_out, kc)."""
+        torch, dev = self.torch, self.dev
+        B = len(windows)
+        nx, nv = self.nx, self.nv
+        rho = self.row[[n - 1 for n in windows]].clone()
+        g = dev.scratch("par_g", (B, nx, nv))
+        flags = []
+        for i, n in enumerate(windows):
+            if n == 1:
+                g[i].copy_(self.g0)
+                flags.append(2)      # true g0, E_prev := E  (parareal.py:169-170,178)
+            else:
+                flags.append(3)      # lifted g, E_prev := E
+        E = torch.empty((B, nx), dtype=torch.float64, device=dev.device)
+        Ep = torch.empty_like(E)
+        kc = torch.ones((B, nx), dtype=torch.uint8, device=dev.device)
+        ki = torch.ones_like(kc)
+        eps = [self.cfg.eps] * B
+        dt = self.kin_p.dt
+        ph0 = make_phase(self.mesh, eps, [dt] * B, [self.sf[n - 1][0] for n in windows])
+        ph1 = make_phase(self.mesh, eps,
+                         [self.sf[n - 1][1] if self.sf[n - 1][1] > 0.0 else dt for n in windows],
+                         [1 if self.sf[n - 1][1] > 0.0 else 0 for n in windows])
+        dev.fine(rho, E, Ep, kc, ki, g, self.rb1.expand(B).contiguous(), flags, [ph0, ph1],
+                 self.knobs, eps, self.rtol_f)
+        return rho, kc
+
+    def iterate(self, k):
+        torch, dev, cfg = self.torch, self.dev, self.cfg
+        ng, nx = cfg.ng, self.nx
+        targets = list(range(k + 1, ng + 1))
+        B = len(targets)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        # this rank's windows: cyclic deal
+        mine = targets[self.comm.rank::self.comm.size]
+        Fall = torch.empty((B, nx), dtype=torch.float64, device=dev.device)
+        fracs = np.zeros(ng + 1)
+        if self.comm.size == 1:
+            Fr, kc = self.fine(targets)
+            Fall.copy_(Fr)
+            kcount = kc.sum(dim=1, dtype=torch.int64)
+        else:
+            per = -(-B // self.comm.size)
+            assert per <= nx, "window share exceeds the gather row width"
+            buf = torch.zeros((per + 1, nx), dtype=torch.float64, device=dev.device)
+            if mine:
+                Fr, kc = self.fine(mine)
+                buf[:len(mine)] = Fr
+                buf[per, :len(mine)] = kc.sum(dim=1, dtype=torch.int64).to(torch.float64)
+            parts = self.comm.all_gather(buf)
+            kcount = torch.empty(B, dtype=torch.int64, device=dev.device)
+            for r, part in enumerate(parts):
+                wins = targets[r::self.comm.size]
+                for j, n in enumerate(wins):
+                    Fall[n - k - 1] = part[j]
+                    kcount[n - k - 1] = part[per, j].to(torch.int64)
+        ev[1].record()
+        delta = torch.empty_like(Fall)
+        dev.jump(Fall, self.G[k + 1:], delta)
+        dev.check()   # NonFiniteState from the jumps (parareal.py:267-269)
+        ev[2].record()
+        new = self.row.clone()
+        Gn = self.G.clone()
+        self._chain(self.row[k], k + 1, ng, new[k + 1:], Gn[k + 1:], delta, self.rtol)
+        ev[3].record()
+        dev.maxdiff(new, self.row, self.err_d)
+        err = float(self.err_d.item())
+        dev.check()   # NonFiniteState after the correction (parareal.py:283-284)
+        for j, n in enumerate(targets):
+            fracs[n] = float(kcount[j].item()) / nx
+        t_fine = ev[0].elapsed_time(ev[1]) * 1e-3
+        t_corr = ev[2].elapsed_time(ev[3]) * 1e-3
+        self.row, self.G = new, Gn
+        return err, delta, fracs, targets, t_fine, t_corr
+
+
+_ENGINES: dict = {}
+
+
+def _engine_for(ledger, cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p):
+    eng = _ENGINES.get(id(ledger))
+    if eng is None or eng.cfg is not cfg:
+        eng = _Engine(cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p)
+        _ENGINES[id(ledger)] = eng
+    return eng
+
+
+# ---------------------------------------------------------------------------
+# reference-facing API
+
+
+def _fine_window(n, rho_in, g0, cfg: PararealConfig, kin_p: KineticStepParams, mesh: PhaseMesh,
+                 rho_bar, ws=None):
+    """F for window n-1 -> n from a boundary density (parareal.py:153-190).
+    The plugin seam: replaceable by monkeypatching this module attribute."""
+    t0, t1 = float(cfg.boundaries[n - 1]), float(cfg.boundaries[n])
+    rtol = field_guard(cfg)
+    E = solve_field(rho_in, rho_bar, mesh, rtol=rtol)
+    tic = time.perf_counter()
+    micro = MicroState(g=g0) if n == 1 else lift(
+        rho_in, E, cfg.eps, mesh, order=cfg.options.lift_order,
+        time_elim=cfg.options.time_elim, rho_bar=rho_bar)
+    t_lift = time.perf_counter() - tic
+    state = HybridState.initial(MacroState(rho=np.asarray(rho_in, float), E=E, t=t0), micro, mesh)
+    tic = time.perf_counter()
+    out = hybrid_propagate(state, t1, kin_p, cfg.thresholds, cfg.options, mesh, rho_bar,
+                           field_rtol=rtol)
+    return out.macro.rho, {"lift_s": t_lift, "fine_s": time.perf_counter() - tic,
+                           "kinetic_fraction": out.labels.kinetic_fraction}
+
+
+_ORIG_FINE_WINDOW = _fine_window
+
+
+def _jump_task(n, row_k, g0, cfg, fluid_p, kin_p, mesh, rho_bar):
+    """parareal.py:193-203 (host seam path)."""
+    rho_in = row_k[n - 1]
+    fine_rho, diag = _fine_window(n, rho_in, g0, cfg, kin_p, mesh, rho_bar)
+    tic = time.perf_counter()
+    coarse = fluid_propagate(MacroState(rho=rho_in, E=np.zeros_like(rho_in),
+                                        t=cfg.boundaries[n - 1]),
+                             cfg.boundaries[n], fluid_p, mesh, rho_bar, field_rtol=field_guard(cfg))
+    diag["fluid_s"] = time.perf_counter() - tic
+    return n, fine_rho - coarse.rho, diag
+
+
+def coarse_sweep(rho0, cfg: PararealConfig, fluid_p: FluidStepParams, mesh: PhaseMesh,
+                 rho_bar: float, g0=None, kin_p=None) -> PararealLedger:
+    """Row 0 from the coarse propagator (parareal.py:210-229), one launch."""
+    tic = time.perf_counter()
+    bounds = cfg.boundaries
+    ledger = PararealLedger(boundaries=bounds, rho=[])
+    if kin_p is None:
+        kin_p = KineticStepParams(eps=cfg.eps, dt=fluid_p.dt)
+    if g0 is None:
+        g0 = np.zeros((mesh.nx,) + mesh.vgrid.shape)
+    eng = _Engine(cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p)
+    eng.coarse_sweep()
+    _ENGINES[id(ledger)] = eng
+    ledger.rho.append(eng.row.cpu().numpy())
+    ledger.kinetic_fraction = np.zeros(cfg.ng + 1)
+    ledger.timings.coarse_sweep = time.perf_counter() - tic
+    return ledger
+
+
+def parareal_iterate(ledger: PararealLedger, k: int, cfg: PararealConfig,
+                     fluid_p: FluidStepParams, kin_p: KineticStepParams, mesh: PhaseMesh,
+                     rho_bar: float, g0, pool=None) -> float:
+    """Consume row k, append row k+1; returns the successive error
+    (parareal.py:232-310)."""
+    iter_tic = time.perf_counter()
+    tm = ledger.timings
+    if _fine_window is not _ORIG_FINE_WINDOW:
+        return _iterate_host_seam(ledger, k, cfg, fluid_p, kin_p, mesh, rho_bar, g0, iter_tic)
+    eng = _ENGINES.get(id(ledger))
+    if eng is None or eng.kin_p is not kin_p or k != len(ledger.rho) - 1:
+        eng = _Engine(cfg, mesh, ledger.rho[0][0], g0, rho_bar, fluid_p, kin_p)
+        eng.row = eng.dev.t(np.ascontiguousarray(ledger.rho[k]))
+        _recompute_G(eng, k)   # G(row_k[n-1]) for the active windows
+        _ENGINES[id(ledger)] = eng
+    err, delta, fracs, targets, t_fine, t_corr = eng.iterate(k)
+    ledger.rho.append(eng.row.cpu().numpy())
+    dh = delta.cpu().numpy()
+    ledger.jumps.append({n: dh[j] for j, n in enumerate(targets)})
+    ledger.err.append(err)
+    for n in targets:
+        ledger.kinetic_fraction[n] = fracs[n]
+    tm.fine_max = max(tm.fine_max, t_fine)
+    tm.fine_total += t_fine
+    tm.fluid_window_max = max(tm.fluid_window_max, t_corr / max(1, len(targets)))
+    tm.correction_total += t_corr
+    tm.iterations.append({"k": k + 1, "err": err, "parallel_s": t_fine, "correction_s": t_corr,
+                          "wall_s": time.perf_counter() - iter_tic})
+    return err
+
+
+def _recompute_G(eng: _Engine, k: int):
+    """G(row_k[n-1]) for n = k+1..Ng as independent chains (cold start)."""
+    torch = eng.torch
+    ng = eng.cfg.ng
+    B = ng - k
+    if B <= 0:
+        return
+    out = torch.empty((B, 1, eng.nx), dtype=torch.float64, device=eng.dev.device)
+    sc = eng.sc[k:ng]
+    eng.dev.chain(eng.row[k:ng].contiguous(), out, None, None, None,
+                  [s[0] for s in sc], [s[1] for s in sc], eng.fluid_p.dt,
+                  eng.rb1.expand(B).contiguous(), eng.rtol_f, m2=eng.fluid_p.m2)
+    eng.G[k + 1:] = out[:, 0]
+    eng.dev.check()
+
+
+def _iterate_host_seam(ledger, k, cfg, fluid_p, kin_p, mesh, rho_bar, g0, iter_tic):
+    """Reference-order iteration through a replaced ``_fine_window``."""
+    row_k = ledger.rho[k]
+    targets = range(k + 1, cfg.ng + 1)
+    tic = time.perf_counter()
+    deltas, diags = {}, {}
+    for n in targets:
+        _, deltas[n], diags[n] = _jump_task(n, row_k, g0, cfg, fluid_p, kin_p, mesh, rho_bar)
+    for n in targets:
+        if not np.isfinite(deltas[n]).all():
+            raise NonFiniteState(f"non-finite fine/coarse jump in window {n} (blow-up)")
+    t_par = time.perf_counter() - tic
+    new_row = row_k.copy()
+    tic = time.perf_counter()
+    zero_E = np.zeros(mesh.nx)
+    for n in targets:
+        coarse = fluid_propagate(MacroState(rho=new_row[n - 1], E=zero_E, t=cfg.boundaries[n - 1]),
+                                 cfg.boundaries[n], fluid_p, mesh, rho_bar,
+                                 field_rtol=field_guard(cfg))
+        new_row[n] = coarse.rho + deltas[n]
+    t_corr = time.perf_counter() - tic
+    if not np.isfinite(new_row).all():
+        raise NonFiniteState(f"non-finite density after parareal iteration {k + 1}")
+    err = float(np.max(np.abs(new_row - row_k)))
+    ledger.rho.append(new_row)
+    ledger.jumps.append(deltas)
+    ledger.err.append(err)
+    for n in targets:
+        ledger.kinetic_fraction[n] = diags[n]["kinetic_fraction"]
+    tm = ledger.timings
+    tm.fine_max = max(tm.fine_max, max((d["fine_s"] for d in diags.values()), default=0.0))
+    tm.fine_total += sum(d["fine_s"] for d in diags.values())
+    tm.lift_max = max(tm.lift_max, max((d["lift_s"] for d in diags.values()), default=0.0))
+    tm.lift_total += sum(d["lift_s"] for d in diags.values())
+    tm.fluid_window_max = max(tm.fluid_window_max,
+                              max((d["fluid_s"] for d in diags.values()), default=0.0))
+    tm.correction_total += t_corr
+    tm.iterations.append({"k": k + 1, "err": err, "parallel_s": t_par, "correction_s": t_corr,
+                          "wall_s": time.perf_counter() - iter_tic})
+    _ENGINES.pop(id(ledger), None)
+    return err
+
+
+def run(cfg: PararealConfig, rho0, g0, mesh: PhaseMesh, rho_bar: float) -> RunResult:
+    """Coarse sweep then parareal iterations (parareal.py:313-353)."""
+    wall_tic = time.perf_counter()
+    E0 = solve_field(rho0, rho_bar, mesh)
+    fluid_p, kin_p = default_params(cfg, mesh, E0)
+    if not cfg.parareal_enabled:
+        result = _serial_fine_run(cfg, rho0, g0, kin_p, mesh, rho_bar)
+        result.ledger.timings.wall_total = time.perf_counter() - wall_tic
+        return result
+    ledger = coarse_sweep(rho0, cfg, fluid_p, mesh, rho_bar, g0=g0, kin_p=kin_p)
+    status = "max_iterations"
+    try:
+        for k in range(cfg.k_max):
+            err = parareal_iterate(ledger, k, cfg, fluid_p, kin_p, mesh, rho_bar, g0)
+            if err < cfg.tol:
+                status = "converged"
+                break
+    finally:
+        _ENGINES.pop(id(ledger), None)
+    ledger.timings.wall_total = time.perf_counter() - wall_tic
+    return RunResult(status=status, iterations=len(ledger.err), ledger=ledger,
+                     boundary_rho=ledger.rho[-1], kinetic_fraction=ledger.kinetic_fraction,
+                     config=cfg)
+
+
+def _serial_fine_run(cfg, rho0, g0, kin_p, mesh, rho_bar) -> RunResult:
+    """Serial fine baseline with state carried across windows (parareal.py:356-392)."""
+    bounds = cfg.boundaries
+    row = np.empty((cfg.ng + 1, mesh.nx))
+    row[0] = rho0
+    fractions = np.zeros(cfg.ng + 1)
+    E0 = solve_field(rho0, rho_bar, mesh)
+    state = HybridState.initial(MacroState(rho=rho0, E=E0, t=0.0), MicroState(g=g0), mesh)
+    tic = time.perf_counter()
+    for n in range(1, cfg.ng + 1):
+        state = hybrid_propagate(state, bounds[n], kin_p, cfg.thresholds, cfg.options, mesh,
+                                 rho_bar, field_rtol=field_guard(cfg))
+        row[n] = state.macro.rho
+        fractions[n] = state.labels.kinetic_fraction
+    ledger = PararealLedger(boundaries=bounds, rho=[row])
+    ledger.kinetic_fraction = fractions
+    ledger.timings.fine_total = time.perf_counter() - tic
+    return RunResult(status="serial", iterations=0, ledger=ledger, boundary_rho=row,
+                     kinetic_fraction=fractions, config=cfg)
+
+
+def lift_restart_reference(cfg, rho0, g0, mesh, rho_bar) -> np.ndarray:
+    """The parareal fixed point: serial chain of lifted restarts (parareal.py:395-413)."""
+    E0 = solve_field(rho0, rho_bar, mesh)
+    _, kin_p = default_params(cfg, mesh, E0)
+    row = np.empty((cfg.ng + 1, mesh.nx))
+    row[0] = rho0
+    for n in range(1, cfg.ng + 1):
+        row[n], _ = _fine_window(n, row[n - 1], g0, cfg, kin_p, mesh, rho_bar)
+    return row
+
+
+@dataclass(frozen=True)
+class PerfModel:
+    t_hmm: float
+    t_fluid: float
+    t_lift: float
+    n_workers: int
+    ng: int
+    k: int
+
+    def __post_init__(self):
+        if min(self.t_hmm, self.t_fluid, self.t_lift) < 0.0:
+            raise ValueError("phase times must be nonnegative")
+        if self.n_workers < 1 or self.ng < 1:
+            raise ValueError("n_workers and ng must be >= 1")
+
+
+def predict_cost(pm: PerfModel):
+    """parareal.py:438-452."""
+    per_iter = (pm.t_lift + pm.t_hmm + pm.t_fluid) / pm.n_workers + pm.t_fluid
+    t_parareal = pm.t_fluid + pm.ng * pm.k * per_iter
+    denom = pm.ng * per_iter
+    k_opt = math.ceil((pm.ng * pm.t_hmm - pm.t_fluid) / denom) if denom > 0.0 else 0
+    return t_parareal, k_opt, t_parareal <= pm.ng * pm.t_hmm

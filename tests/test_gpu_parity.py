@@ -1,0 +1,375 @@
+"""Device (libpk) vs oracle / golden vectors.  Exact mode: bitwise equality
+(np.array_equal, i.e. equal up to the sign of zero)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from _cases import HYB_CASES, PAR_CASES, digest, f_paper
+
+pytestmark = pytest.mark.gpu
+
+pk = pytest.importorskip("paper_2511_13386_b200")
+from paper_2511_13386_b200 import configs  # noqa: E402
+from paper_2511_13386_b200.adaptation import DomainLabels  # noqa: E402
+
+
+def eq(a, b):
+    return np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def mesh(nx, nv, vs=8.0):
+    return pk.build_mesh(pk.MeshSpec(nx=nx, nvx=nv, v_star=vs))
+
+
+def g4(m, g2):
+    return np.asarray(g2).reshape((m.nx, m.nv, 1, 1))
+
+
+def test_native_loaded():
+    from paper_2511_13386_b200 import _native
+
+    assert _native.load()._name.endswith("libpk.so")
+
+
+@pytest.mark.parametrize("nx", [16, 128, 1000, 8192])
+def test_field(gold, nx):
+    d = gold("field")
+    m = mesh(nx, 8)
+    assert eq(pk.solve_field(d[f"rho_{nx}"], 2.0, m), d[f"E_{nx}"])
+
+
+def test_field_guard(gold):
+    d = gold("field")
+    with pytest.raises(pk.SolvabilityViolation):
+        pk.solve_field(d["guard_rho"], 2.0, mesh(64, 8))
+
+
+def test_kinetic_cfg1_golden(gold):
+    """BASELINE cfg1 in full (128x64, eps=1, dt=1e-3, 200 steps) vs the reference."""
+    d = gold("kinetic")
+    c = configs.cfg1()
+    m = c.mesh
+    st = (pk.MacroState(c.rho, np.zeros(m.nx), 0.0), pk.MicroState(c.g))
+    mac, mic = pk.kinetic_propagate(st, 0.2, pk.KineticStepParams(eps=1.0, dt=1e-3), m, c.rho_bar)
+    assert eq(mac.rho, d["c1_rho"]) and eq(mac.E, d["c1_E"])
+    assert eq(mic.g.reshape(128, 64), d["c1_g"])
+    assert mac.t == 0.2
+
+
+@pytest.mark.parametrize("eps", [0.5, 1e-4])
+def test_kinetic_remainder_golden(gold, eps):
+    d = gold("kinetic")
+    m = mesh(32, 32)
+    grid = O.make_grid(32, 32)
+    rho, g0, rb = O.decompose(f_paper(grid.vx, grid.M, grid.x_star), grid)
+    E0 = pk.solve_field(rho, rb, m)
+    p = pk.KineticStepParams.default(m, eps, e_max=float(np.abs(E0).max()))
+    k = f"p_{eps:g}"
+    assert eq([p.dt, 37.5 * p.dt], d[k + "_dt"])
+    mac, mic = pk.kinetic_propagate((pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0))),
+                                    37.5 * p.dt, p, m, rb)
+    assert eq(mac.rho, d[k + "_rho"]) and eq(mac.E, d[k + "_E"])
+    assert eq(mic.g.reshape(32, 32), d[k + "_g"])
+
+
+@pytest.mark.parametrize("nx,nv", [(64, 64), (128, 128), (96, 256), (48, 512), (40, 16),
+                                   (33, 9), (64, 32), (24, 200)])
+def test_kinetic_layouts_vs_oracle(nx, nv):
+    """Every row layout (fast nv = 64/128/256/512, generic otherwise) bitwise."""
+    m = mesh(nx, nv)
+    grid = O.make_grid(nx, nv)
+    rho, g0, rb = O.decompose(f_paper(grid.vx, grid.M, grid.x_star), grid)
+    E0 = O.field(rho, rb, grid)
+    for eps in (0.7, 3e-3):
+        dt = O.stable_dt(grid, eps, e_max=float(np.abs(E0).max()))
+        r, E, gg = O.kinetic_advance(rho, g0, 0.0, 12.5 * dt, dt, eps, grid, rb)
+        mac, mic = pk.kinetic_propagate((pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0))),
+                                        12.5 * dt, pk.KineticStepParams(eps=eps, dt=dt), m, rb)
+        assert eq(mac.rho, r), (nx, nv, eps)
+        assert eq(mac.E, E)
+        assert eq(mic.g.reshape(nx, nv), gg)
+
+
+def test_kinetic_cfg5_instances_golden(gold):
+    d = gold("kinetic")
+    for s in (0, 1):
+        c = configs.cfg5([s])[0]
+        m = c.mesh
+        rb, eps, dt = d[f"c5_{s}_par"]
+        E0 = pk.solve_field(c.rho, rb, m)
+        p = pk.KineticStepParams.default(m, eps, e_max=float(np.abs(E0).max()))
+        assert p.dt == dt
+        st = (pk.MacroState(c.rho, E0, 0.0), pk.MicroState(c.g))
+        mac, mic = pk.kinetic_propagate(st, 5 * dt, p, m, rb)
+        # 5*dt spans exactly 5 steps only if no remainder appears; use steps
+        n_full, rem = pk.fluid.substep_sizes(0.0, 5 * dt, dt)
+        if (n_full, rem) == (5, 0.0):
+            assert eq(mac.rho, d[f"c5_{s}_rho"]) and eq(mac.E, d[f"c5_{s}_E"])
+            assert digest(mic.g.reshape(1024, 128)) == str(d[f"c5_{s}_g"])
+        st = (pk.MacroState(c.rho, E0, 0.0), pk.MicroState(c.g))
+        for _ in range(5):
+            st = pk.kinetic_step(st, p, m, rb)
+        assert eq(st[0].rho, d[f"c5_{s}_rho"]) and eq(st[0].E, d[f"c5_{s}_E"])
+        assert digest(st[1].g.reshape(1024, 128)) == str(d[f"c5_{s}_g"])
+
+
+def _hyb_in(d, name, nx, nv):
+    v = d["h_" + name + "_in"]
+    n = nx * nv
+    return v[:nx], v[nx:nx + n].reshape(nx, nv), v[nx + n], v[nx + n + 1], v[nx + n + 2]
+
+
+@pytest.mark.parametrize("case", HYB_CASES, ids=[c[0] for c in HYB_CASES])
+def test_hybrid_golden(gold, case):
+    """Adaptation on: labels every step, flips (lift / zero), masked update,
+    stale neighbours, guard — bitwise vs the reference."""
+    name, data, nx, nv, eps, d0, e0, kw, nsteps, rtol = case
+    d = gold("hybrid")
+    rho, g0, rb, dt, t_end = _hyb_in(d, name, nx, nv)
+    m = mesh(nx, nv)
+    E0 = pk.solve_field(rho, rb, m)
+    p = pk.KineticStepParams(eps=eps, dt=dt)
+    st = pk.HybridState.initial(pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0)), m)
+    opts = pk.HybridOptions(**kw)
+    th = pk.Thresholds(d0, e0)
+    k = "h_" + name
+    if k + "_raised" in d.files:
+        with pytest.raises(pk.SolvabilityViolation):
+            pk.hybrid_propagate(st, t_end, p, th, opts, m, rb, field_rtol=rtol)
+        return
+    out = pk.hybrid_propagate(st, t_end, p, th, opts, m, rb, field_rtol=rtol)
+    assert eq(out.macro.rho, d[k + "_rho"])
+    assert eq(out.macro.E, d[k + "_E"])
+    assert eq(out.micro.g.reshape(nx, nv), d[k + "_g"])
+    assert eq(out.labels.kinetic_cells, d[k + "_kc"])
+    assert eq(out.labels.kinetic_ifaces, d[k + "_ki"])
+    assert eq(out.E_prev, d[k + "_Eprev"])
+
+
+def test_hybrid_trace_path(gold):
+    """The per-substep trace callback (slow path) sees the reference's labels."""
+    name, data, nx, nv, eps, d0, e0, kw, nsteps, rtol = HYB_CASES[3]
+    d = gold("hybrid")
+    rho, g0, rb, dt, t_end = _hyb_in(d, name, nx, nv)
+    m = mesh(nx, nv)
+    E0 = pk.solve_field(rho, rb, m)
+    st = pk.HybridState.initial(pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0)), m)
+    trace = []
+    t_short = 30.5 * dt
+    pk.hybrid_propagate(st, t_short, pk.KineticStepParams(eps=eps, dt=dt),
+                        pk.Thresholds(d0, e0), pk.HybridOptions(**kw), m, rb,
+                        trace=lambda s: trace.append(s.labels.kinetic_cells.copy()),
+                        field_rtol=rtol)
+    assert eq(np.array(trace), d["h_" + name + "_trace"][:len(trace)])
+
+
+def test_lift_golden(gold):
+    d = gold("lift")
+    m = mesh(64, 32)
+    rho, E, E_prev, rb = d["rho"], d["E"], d["E_prev"], float(d["rb"])
+    for eps in (0.5, 1e-3):
+        for order in (1, 2):
+            for te in ("leading", "higher_order"):
+                for proj in (True, False):
+                    g = pk.lift(rho, E, eps, m, order=order, time_elim=te, rho_bar=rb,
+                                dE_dt=(E - E_prev) / 1e-4, project=proj)
+                    assert eq(g.g.reshape(64, 32), d[f"l_{eps:g}_{order}_{te}_{int(proj)}"])
+
+
+def test_lift_errors():
+    m = mesh(16, 8)
+    with pytest.raises(ValueError):
+        pk.lift(np.ones(16), np.zeros(16), 0.5, m, order=3)
+    with pytest.raises(ValueError):
+        pk.lift(np.ones(16), np.zeros(16), 0.5, m, time_elim="bogus")
+
+
+def test_fluid_golden(gold):
+    d = gold("fluid")
+    m = mesh(256, 64)
+    fp = pk.FluidStepParams.default(m)
+    assert fp.dt == float(d["dt"])
+    st = pk.fluid_propagate(pk.MacroState(d["rho0"], np.zeros(256), 0.0), 0.5 / 16, fp, m,
+                            float(d["rb"]))
+    assert eq(st.rho, d["rho"]) and eq(st.E, d["E"])
+
+
+def test_fluid_step_matches_oracle():
+    m = mesh(40, 8)
+    grid = O.make_grid(40, 8)
+    rho = 1.0 + 0.2 * np.cos(grid.x_centers)
+    rb = float(rho.sum() * grid.dx / grid.x_star)
+    E = O.field(rho, rb, grid)
+    fp = pk.FluidStepParams.default(m)
+    st = pk.fluid_step(pk.MacroState(rho, E, 0.0), fp, m, rb)
+    J = O.flux_J(rho, E, grid)
+    r1 = O.rho_fluid(rho, J, grid.m2, fp.dt, grid)
+    assert eq(st.rho, r1) and eq(st.E, O.field(r1, rb, grid))
+
+
+@pytest.mark.parametrize("case", PAR_CASES, ids=[c[0] for c in PAR_CASES])
+def test_parareal_small_golden(gold, case):
+    name, nx, nv, eps, adapt, ng, T, kmax, tol, d0, e0 = case
+    d = gold("parareal")
+    m = mesh(nx, nv)
+    grid = O.make_grid(nx, nv)
+    rho, g0, rb = O.decompose(f_paper(grid.vx, grid.M, grid.x_star), grid)
+    cfg = pk.PararealConfig(eps=eps, t_final=T, ng=ng, k_max=kmax, tol=tol,
+                            thresholds=pk.Thresholds(d0, e0),
+                            options=pk.HybridOptions(adaptation=adapt))
+    k = f"p_{name}"
+    if k + "_raised" in d.files:
+        with pytest.raises(pk.SolvabilityViolation):
+            pk.run(cfg, rho, g4(m, g0), m, rb)
+        return
+    res = pk.run(cfg, rho, g4(m, g0), m, rb)
+    assert eq(np.stack(res.ledger.rho), d[k + "_rows"])
+    assert eq(res.ledger.err, d[k + "_err"])
+    assert eq(res.kinetic_fraction, d[k + "_frac"])
+    assert [res.iterations, res.status == "converged"] == list(d[k + "_meta"])
+
+
+def test_parareal_cfg2_golden(gold):
+    """BASELINE cfg2 end to end: iteration count 4 and every ledger row bitwise
+    equal to the reference run."""
+    d = gold("parareal")
+    c = configs.cfg2()
+    cfg = pk.PararealConfig(eps=1e-2, t_final=0.5, ng=16, k_max=5, tol=1e-10,
+                            options=pk.HybridOptions(adaptation=False))
+    res = pk.run(cfg, c.rho, c.g, c.mesh, c.rho_bar)
+    assert res.status == "converged" and res.iterations == 4
+    assert eq(np.stack(res.ledger.rho), d["c2_rows"])
+    assert eq(res.ledger.err, d["c2_err"])
+
+
+def test_fine_window_seam_monkeypatch(monkeypatch):
+    """The reference's plugin seam: replacing _fine_window by the coarse
+    propagator converges in one iteration with err == 0 (test_parareal.py:51-69)."""
+    import paper_2511_13386_b200.parareal as ppl
+
+    m = mesh(16, 8)
+    grid = O.make_grid(16, 8)
+    rho, g0, rb = O.decompose(f_paper(grid.vx, grid.M, grid.x_star), grid)
+
+    def fake_fine(n, rho_in, g0, cfg, kin_p, mesh, rho_bar, ws=None):
+        fp = pk.FluidStepParams.default(mesh)
+        out = pk.fluid_propagate(pk.MacroState(rho_in, np.zeros_like(rho_in),
+                                               cfg.boundaries[n - 1]),
+                                 cfg.boundaries[n], fp, mesh, rho_bar)
+        return out.rho, {"lift_s": 0.0, "fine_s": 0.0, "kinetic_fraction": 0.0}
+
+    monkeypatch.setattr(ppl, "_fine_window", fake_fine)
+    cfg = pk.PararealConfig(eps=0.5, t_final=0.2, ng=6, k_max=12,
+                            options=pk.HybridOptions(adaptation=False))
+    res = pk.run(cfg, rho, g4(m, g0), m, rb)
+    assert res.status == "converged" and res.iterations == 1 and res.ledger.err[0] == 0.0
+
+
+def test_batched_fine_matches_serial_windows():
+    """B slices in one launch == each slice alone (cfg5-type instances)."""
+    import torch
+
+    from paper_2511_13386_b200.engine import Device, HybridKnobs, make_phase
+
+    cases = configs.cfg5(range(6), nx=128, nv=128)
+    m = cases[0].mesh
+    dev = Device.for_mesh(m)
+    grid = O.make_grid(128, 128)
+    B = len(cases)
+    rho = dev.t(np.stack([c.rho for c in cases]))
+    g = dev.t(np.stack([c.g.reshape(128, 128) for c in cases]))
+    E = torch.zeros_like(rho)
+    Ep = torch.zeros_like(rho)
+    kc = torch.ones((B, 128), dtype=torch.uint8, device=dev.device)
+    ki = torch.ones_like(kc)
+    rbs = dev.t(np.array([c.rho_bar for c in cases]))
+    eps = [c.eps for c in cases]
+    dts = []
+    for c in cases:
+        E0 = O.field(c.rho, c.rho_bar, grid)
+        dts.append(O.stable_dt(grid, c.eps, e_max=float(np.abs(E0).max())))
+    ph0 = make_phase(m, eps, dts, [20] * B)
+    ph1 = make_phase(m, eps, dts, [0] * B)
+    dev.fine(rho, E, Ep, kc, ki, g, rbs, [0] * B, [ph0, ph1], HybridKnobs(), eps, 1e-10)
+    dev.check()
+    for b, c in enumerate(cases):
+        r, EE, gg = O.kinetic_steps(c.rho, c.g.reshape(128, 128), 20, dts[b], c.eps, grid,
+                                    c.rho_bar)
+        assert eq(rho[b].cpu().numpy(), r)
+        assert eq(E[b].cpu().numpy(), EE)
+        assert eq(g[b].cpu().numpy(), gg)
+
+
+def test_eps_profile_hybrid_vs_oracle():
+    """eps(x) extension (cfg3 profile) on a reduced grid: device == oracle restatement."""
+    nx, nv = 64, 64
+    m = mesh(nx, nv)
+    grid = O.make_grid(nx, nv)
+    prof_pk = pk.EpsProfile.from_function(configs.eps_bump, m)
+    prof_o = O.EpsProfile.from_function(configs.eps_bump, grid)
+    rho, _, rb = O.decompose(lambda x: (1.0 + 0.5 * np.cos(x))[:, None] * grid.M[None, :], grid)
+    E0 = O.field(rho, rb, grid)
+    g0 = O.lift(rho, E0, prof_o, grid, rho_bar=rb)
+    assert eq(pk.lift(rho, E0, prof_pk, m, rho_bar=rb).g.reshape(nx, nv), g0)
+    dt = O.stable_dt(grid, prof_o, e_max=float(np.abs(E0).max()))
+    assert pk.stable_dt(m, prof_pk, e_max=float(np.abs(E0).max())) == dt
+    st_o = O.HState.start(rho, E0, g0)
+    ref = O.hpropagate(st_o, 60.5 * dt, dt, prof_o, 1e-3, 1e-3, O.HOpts(), grid, rb, 1e-2)
+    st = pk.HybridState.initial(pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0)), m)
+    out = pk.hybrid_propagate(st, 60.5 * dt, pk.KineticStepParams(eps=prof_pk, dt=dt),
+                              pk.Thresholds(1e-3, 1e-3), pk.HybridOptions(), m, rb,
+                              field_rtol=1e-2)
+    assert 0.0 < ref.kc.mean() < 1.0, "expected a mixed partition"
+    assert eq(out.macro.rho, ref.rho) and eq(out.micro.g.reshape(nx, nv), ref.g)
+    assert eq(out.labels.kinetic_cells, ref.kc)
+
+
+def test_all_kinetic_hybrid_equals_kinetic():
+    """tests/test_hybrid.py:17-28 on the device: 100 steps, bitwise."""
+    m = mesh(32, 64)
+    grid = O.make_grid(32, 64)
+    rho, g0, rb = O.decompose(f_paper(grid.vx, grid.M, grid.x_star), grid)
+    E0 = pk.solve_field(rho, rb, m)
+    p = pk.KineticStepParams.default(m, 0.5, e_max=float(np.abs(E0).max()))
+    hyb = pk.HybridState.initial(pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0)), m)
+    hyb = pk.hybrid_propagate(hyb, 100 * p.dt, p, pk.Thresholds(1e-5, 1e-5),
+                              pk.HybridOptions(adaptation=False), m, rb)
+    kin = pk.kinetic_propagate((pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0))),
+                               100 * p.dt, p, m, rb)
+    assert eq(hyb.macro.rho, kin[0].rho) and eq(hyb.micro.g, kin[1].g)
+    assert hyb.labels.kinetic_cells.all()
+
+
+def test_stale_neighbour_semantics():
+    """a kinetic interface reads a neighbour that flipped to fluid
+    this step with its stored (non-zero) perturbation."""
+    nx, nv = 32, 64
+    m = mesh(nx, nv)
+    grid = O.make_grid(nx, nv)
+    rho, g0, rb = O.decompose(f_paper(grid.vx, grid.M, grid.x_star), grid)
+    E0 = O.field(rho, rb, grid)
+    dt = O.stable_dt(grid, 1e-2, e_max=float(np.abs(E0).max()))
+    # previous labels all kinetic; thresholds chosen so some cells go fluid at step 1
+    st_o = O.HState.start(rho, E0, g0)
+    ref = O.hstep(st_o, dt, 1e-2, 1e-3, 1e-3, O.HOpts(), grid, rb, 1e-2)
+    assert 0 < ref.ki.sum() < nx
+    st = pk.HybridState.initial(pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0)), m)
+    out = pk.hybrid_step(st, pk.KineticStepParams(eps=1e-2, dt=dt), pk.Thresholds(1e-3, 1e-3),
+                         pk.HybridOptions(), m, rb, field_rtol=1e-2)
+    assert eq(out.macro.rho, ref.rho) and eq(out.micro.g.reshape(nx, nv), ref.g)
+    assert eq(out.labels.kinetic_ifaces, ref.ki)
+
+
+def test_invalid_reinit_raises_on_flip():
+    nx, nv = 16, 8
+    m = mesh(nx, nv)
+    grid = O.make_grid(nx, nv)
+    rho, g0, rb = O.decompose(f_paper(grid.vx, grid.M, grid.x_star), grid)
+    E0 = pk.solve_field(rho, rb, m)
+    p = pk.KineticStepParams.default(m, 1e-4, e_max=float(np.abs(E0).max()))
+    st = pk.HybridState(pk.MacroState(rho, E0, 0.0), pk.MicroState(g4(m, g0)),
+                        DomainLabels.all_fluid(nx), E0)
+    with pytest.raises(ValueError):
+        pk.hybrid_step(st, p, pk.Thresholds(1e-5, 1e-5), pk.HybridOptions(reinit="nearest"),
+                       m, rb, field_rtol=1e-5)
