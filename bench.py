@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark: micro-macro phase-space cell-updates/s of the fine solver F.
+
+Workload (BASELINE.json configs[4], the largest single-GPU throughput config):
+256 seeded instances, Nx=1024, Nv=128, eps log-uniform in [1e-4, 1], 500
+kinetic steps each at the reference's stable dt.  One bench "step" = one pass
+of the hot path over the whole batch (256 x 500 x 1024 x 128 = 1.68e10
+cell-updates).  Under torchrun the instances are partitioned across ranks
+(strong scaling, no data-path collective).  Also reported: cfg2 parareal wall
+time (BASELINE configs[1]) on this GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "micro-macro cell-updates/s (fine solver)"
+UNIT = "cell-updates/s"
+NINST, NX, NV, NSTEPS = 256, 1024, 128, 500
+BYTES_PER_UPDATE = 16  # read g once, write g once, fp64
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_inputs(instances):
+    from paper_2511_13386_b200 import configs
+    from paper_2511_13386_b200.kinetic import stable_dt
+    from paper_2511_13386_b200.poisson import solve_field
+
+    cases = configs.cfg5(instances, nx=NX, nv=NV)
+    m = cases[0].mesh
+    rho = np.stack([c.rho for c in cases])
+    g = np.stack([c.g.reshape(NX, NV) for c in cases])
+    eps = [c.eps for c in cases]
+    rb = [c.rho_bar for c in cases]
+    dts = []
+    for c in cases:
+        E0 = solve_field(c.rho, c.rho_bar, m)
+        dts.append(stable_dt(m, c.eps, e_max=float(np.max(np.abs(E0)))))
+    return m, cases, rho, g, eps, rb, dts
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle (numpy restatement of the reference, CPU port)
+
+
+def _cpu_job(args):
+    s, nsteps = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import oracle as O
+    from paper_2511_13386_b200 import configs
+
+    c = configs.cfg5([s], nx=NX, nv=NV)[0]
+    grid = O.make_grid(NX, NV)
+    E0 = O.field(c.rho, c.rho_bar, grid)
+    dt = O.stable_dt(grid, c.eps, e_max=float(np.abs(E0).max()))
+    g = c.g.reshape(NX, NV)
+    t0 = time.perf_counter()
+    O.kinetic_steps(c.rho, g, nsteps, dt, c.eps, grid, c.rho_bar)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(n_inst=None, nsteps=40):
+    """Oracle on a bounded sample: one instance per process, all host cores."""
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    procs = min(cores, 64)
+    n_inst = n_inst or procs
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(procs) as pool:
+        pool.map(_cpu_job, [(s, nsteps) for s in range(n_inst)])
+    wall = time.perf_counter() - t0
+    upd = n_inst * nsteps * NX * NV
+    return {"value": upd / wall, "unit": UNIT, "cores": procs, "kind": "port",
+            "sample": f"{n_inst} cfg5 instances x {nsteps} steps (1024x128), one numpy "
+                      f"process per instance, wall {wall:.2f} s incl. pool start"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    steps, warm = args.steps, args.warmup
+    per = []
+    for i in range(warm + steps):
+        cb = cpu_baseline(nsteps=20)
+        if i >= warm:
+            per.append(cb["value"])
+    v = statistics.median(per)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+            "steps": steps, "warmup": warm, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg5 ensemble: 256 x (1024x128), 500 kinetic steps; "
+                                   "reference arm = oracle CPU port on a bounded sample"},
+            "cpu_baseline": {**cb, "value": v},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parareal", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev_index = torch.cuda.current_device()
+
+    from paper_2511_13386_b200.ensemble import Ensemble
+
+    mine = list(range(NINST))[rank::ws] if ws > 1 else list(range(NINST))
+    m, cases, rho0, g0, eps, rb, dts = build_inputs(mine)
+    B = len(mine)
+    ens = Ensemble(m, eps, dts, rb)
+    rho_d = torch.from_numpy(rho0).cuda()
+    g_d = torch.from_numpy(g0).cuda()
+    upd_rank = B * NSTEPS * NX * NV
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def maxr(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (untimed)
+    for _ in range(args.warmup):
+        ens.load(rho_d, g_d)
+        ens.run(NSTEPS)
+    barrier()
+    # timed region: device-resident inputs (restored on device each step)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev_index) as clk:
+        barrier()
+        t0.record()
+        for i in range(args.steps):
+            starts[i].record()
+            ens.load(rho_d, g_d)
+            kstart[i].record()
+            ens.run(NSTEPS, check=False)
+            ends[i].record()
+        t1.record()
+        barrier()
+    ens.dev.check()
+    total_ms = maxr(t0.elapsed_time(t1))
+    kern_ms = [kstart[i].elapsed_time(ends[i]) for i in range(args.steps)]
+    kern_avg = maxr(sum(kern_ms) / len(kern_ms))
+    ms_step = total_ms / args.steps
+    value = upd_rank * ws * args.steps / (total_ms * 1e-3)
+    peak, peak_src = peaks()
+    achieved = upd_rank * BYTES_PER_UPDATE / (kern_avg * 1e-3) / 1e9
+
+    # e2e: public host-array API semantics, pinned host buffers, copies timed
+    rho_h = torch.from_numpy(rho0).pin_memory()
+    g_h = torch.from_numpy(g0).pin_memory()
+    rho_o = torch.empty_like(rho_h).pin_memory()
+    E_o = torch.empty_like(rho_h).pin_memory()
+    g_o = torch.empty_like(g_h).pin_memory()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        ens.load(rho_h, g_h, non_blocking=True)
+        ens.run(NSTEPS, check=False)
+        rho_o.copy_(ens.rho, non_blocking=True)
+        E_o.copy_(ens.E, non_blocking=True)
+        g_o.copy_(ens.g, non_blocking=True)
+    e1.record()
+    barrier()
+    ens.dev.check()
+    e2e_ms = maxr(e0.elapsed_time(e1))
+    e2e = upd_rank * ws * args.steps / (e2e_ms * 1e-3)
+    h2d = (rho_h.numel() + g_h.numel()) * 8 * ws
+    d2h = (rho_o.numel() * 2 + g_o.numel()) * 8 * ws
+
+    extra = {}
+    if rank == 0 and not args.no_parareal:
+        extra["parareal"] = parareal_cfg2()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "fine_kernel_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr = json.load(f)
+        if tr.get("nv") == NV and tr.get("nx") == NX:
+            traffic = tr.get("bytes_per_update")
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg5 ensemble: 256 seeded instances x (Nx=1024, Nv=128), "
+                                   "500 kinetic steps at the reference stable dt",
+                       "instances": NINST, "nx": NX, "nv": NV, "steps_per_instance": NSTEPS,
+                       "cell_updates_per_step": NINST * NSTEPS * NX * NV,
+                       "parallelism": f"instances/{ws} per GPU" if ws > 1 else "1 GPU",
+                       "l2": "inputs (2 x 256 MiB g buffers) larger than L2",
+                       "mode": "exact (bitwise vs reference)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "traffic": traffic,
+                         "algorithmic_bytes_per_update": BYTES_PER_UPDATE,
+                         "kernel_ms": kern_avg},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            **extra,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def parareal_cfg2():
+    """BASELINE configs[1] wall time on this GPU through the drop-in run()."""
+    import torch
+
+    import paper_2511_13386_b200 as pk
+    from paper_2511_13386_b200 import configs
+
+    c = configs.cfg2()
+    cfg = pk.PararealConfig(eps=1e-2, t_final=0.5, ng=16, k_max=5, tol=1e-10,
+                            options=pk.HybridOptions(adaptation=False))
+    pk.run(cfg, c.rho, c.g, c.mesh, c.rho_bar)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = pk.run(cfg, c.rho, c.g, c.mesh, c.rho_bar)
+    wall = time.perf_counter() - t0
+    tm = res.ledger.timings
+    E0 = pk.solve_field(c.rho, c.rho_bar, c.mesh)
+    _, kin_p = pk.parareal.default_params(cfg, c.mesh, E0)
+    nf, rem = pk.fluid.substep_sizes(0.0, 0.5 / 16, kin_p.dt)
+    per_window = (nf + (1 if rem > 0.0 else 0)) * 256 * 64
+    fine_updates = sum(16 - k for k in range(res.iterations)) * per_window
+    return {"config": "cfg2: Nx=256, Nv=64, eps=1e-2, T=0.5, 16 slices, reference dt",
+            "wall_s": wall, "iterations": res.iterations, "status": res.status,
+            "fine_s": tm.fine_total, "correction_s": tm.correction_total,
+            "coarse_sweep_s": tm.coarse_sweep,
+            "fine_cell_updates": fine_updates,
+            "fine_cell_updates_per_s": fine_updates / max(tm.fine_total, 1e-12),
+            "reference_cpu_s_build_container_1core": 41.7}
+
+
+if __name__ == "__main__":
+    main()

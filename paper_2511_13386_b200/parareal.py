@@ -243,6 +243,10 @@ class _Engine:
         ng, nx = cfg.ng, self.nx
         targets = list(range(k + 1, ng + 1))
         B = len(targets)
+        if B == 0:
+            # every window converged by prefix exactness: row_{k+1} == row_k
+            return 0.0, torch.empty((0, nx), dtype=torch.float64, device=dev.device), \
+                np.zeros(ng + 1), targets, 0.0, 0.0
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record()
         # this rank's windows: cyclic deal
