@@ -93,6 +93,10 @@ const char* pk_last_error(const pk_ctx* ctx);
 int32_t pk_reserve(pk_ctx* ctx, int32_t max_slices);              /* grow scratch */
 int32_t pk_status_read(pk_ctx* ctx, pk_status* out, int32_t clear); /* synchronises */
 int32_t pk_version(void);
+/* diagnostics: accumulate per-phase clock64 counters of slice 0 into a device
+ * array of 6 int64 [micro, barrier, slice finish, slice prepare, barrier,
+ * steps]; NULL disables. */
+int32_t pk_debug_profile(pk_ctx* ctx, void* dev_counters);
 
 /* --- fine propagator F --------------------------------------------------
  * B independent slices, each advanced through phases[0] then phases[1]

@@ -55,6 +55,7 @@ class PkStatus(C.Structure):
 # symbol -> (restype, argtypes); the full C ABI of include/pk.h
 SIGNATURES = {
     "pk_version": (C.c_int32, []),
+    "pk_debug_profile": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "pk_create": (C.c_void_p, [C.c_int32, C.POINTER(PkMesh)]),
     "pk_destroy": (None, [C.c_void_p]),
     "pk_last_error": (C.c_char_p, [C.c_void_p]),

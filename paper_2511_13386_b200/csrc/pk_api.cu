@@ -38,6 +38,7 @@ struct pk_ctx {
   int8_t* i8ws = nullptr;
   uint8_t* u8ws = nullptr;  // 7 arrays
   int* iws = nullptr;       // klist cap*nx, nk cap, abort cap
+  long long* prof = nullptr;  // optional device phase counters (pk_debug_profile)
   std::string err;
 };
 
@@ -146,7 +147,7 @@ void bind_ws(pk_ctx* c, pk::FineArgs& a) {
   const size_t n = (size_t)c->cap * c->m.nx;
   double* d = c->dws;
   double** dst[NDWS] = {&a.J, &a.fl, &a.sq, &a.bm, &a.dco, &a.vco, &a.tA, &a.tB,
-                        &a.tC, &a.tD, &a.tE, &a.blift, nullptr, nullptr, nullptr, nullptr};
+                        &a.tC, &a.tD, &a.tE, &a.blift, &a.lJ, nullptr, nullptr, nullptr};
   for (int i = 0; i < NDWS; ++i)
     if (dst[i]) *dst[i] = d + i * n;
   a.vsg = c->i8ws;
@@ -160,6 +161,7 @@ void bind_ws(pk_ctx* c, pk::FineArgs& a) {
   a.nk = c->iws + n;
   a.abort_ = c->iws + n + c->cap;
   a.status = c->d_status;
+  a.prof = c->prof;
 }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -169,6 +171,12 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 extern "C" {
 
 int32_t pk_version(void) { return 1; }
+
+int32_t pk_debug_profile(pk_ctx* c, void* dev_counters) {
+  if (!c) return PK_ERR_BAD_ARG;
+  c->prof = reinterpret_cast<long long*>(dev_counters);
+  return PK_OK;
+}
 
 pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   if (!mesh || mesh->nx < 7 || mesh->nv < 1) return nullptr;

@@ -51,18 +51,20 @@ struct FineArgs {
   PhaseDev ph[2];
   // hybrid options (hybrid.py:45-55)
   int adaptation, combine_and, reinit, lift_order, time_elim, exact_scan;
+  int local_smem;         // leader slice vectors in shared memory (set by the launcher)
   double delta0, eta0, rtol;
   const double* rscale;  // [B*nx] eps_c^2 for scale_remainder, or null
   const double* neg_eps; // [B*nx] -eps_i
   const double* eps2;    // [B*nx] eps_i^2
   // workspace [B*nx] unless noted
-  double *J, *fl, *sq, *bm, *dco, *vco, *tA, *tB, *tC, *tD, *tE, *blift;
+  double *J, *fl, *sq, *bm, *dco, *vco, *tA, *tB, *tC, *tD, *tE, *blift, *lJ;
   int8_t* vsg;
   uint8_t *flip, *nza, *nzb, *kcn, *kin;
   int* klist;
   int* nk;               // [B]
   int* abort_;           // [B]
   Status* status;
+  long long* prof;       // [6] optional phase profile (pk_debug_profile), or null
 };
 
 struct LiftArgs {

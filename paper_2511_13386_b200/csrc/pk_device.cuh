@@ -88,27 +88,38 @@ __device__ double block_pairwise(F x, const PwPlan& P, double* scratch) {
   return res;
 }
 
-// Sequential prefix sum (np.cumsum order) of src into dst by warp 0 of the
-// block; values are staged 32 at a time and shuffled to every lane so the
-// only serial dependency is the add chain.  Other warps return immediately.
+// Sequential prefix sum (np.cumsum order) of src into dst by thread 0 of the
+// block.  The operands are software-pipelined through registers (the next
+// block of 16 is loaded before the current block's adds and stores), so the
+// only serial dependency is the add chain itself.  Other threads return.
 template <class FS, class FD>
 __device__ __forceinline__ void warp_cumsum(FS src, FD dst, int n) {
-  if ((threadIdx.x >> 5) != 0) return;
-  const int lane = threadIdx.x & 31;
+  if (threadIdx.x != 0) return;
+  constexpr int K = 16;
   double acc = -0.0;  // -0.0 + t == t bitwise: out[0] = src[0]
-  for (int base = 0; base < n; base += 32) {
-    const int m = min(32, n - base);
-    const double v = (lane < m) ? src(base + lane) : 0.0;
-    double mine = 0.0;
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
-      if (j < m) {
-        const double t = __shfl_sync(FULL, v, j);
-        acc = acc + t;
-        if (lane == j) mine = acc;
-      }
+  const int nk = n - n % K;
+  double cur[K];
+  if (nk > 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) cur[k] = src(k);
+  }
+  for (int i = 0; i < nk; i += K) {
+    double nxt[K];
+    if (i + K < nk) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) nxt[k] = src(i + K + k);
     }
-    if (lane < m) dst(base + lane, mine);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      acc = acc + cur[k];
+      dst(i + k, acc);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) cur[k] = nxt[k];
+  }
+  for (int i = nk; i < n; ++i) {
+    acc = acc + src(i);
+    dst(i, acc);
   }
 }
 

@@ -2,277 +2,94 @@
 // whole window (all steps) in a single persistent launch.
 //
 // Per step (hybrid.py:123-188, kinetic.py:255-273):
-//   micro phase   all CTAs of the cluster, one warp per interface row:
+//   micro phase   every warp of the cluster streams its share of the kinetic
+//                 interface rows: TMA bulk copies (cp.async.bulk + mbarrier)
+//                 feed a per-warp shared-memory ring, the warp computes
 //                 g' = k1 g - k2 (upwind transport - M d_x<xi g> + xi M J)
-//                 (kinetic.py:148-224) and the row moments <xi g'>, <g'^2>;
-//                 only kinetic rows are visited (compacted row list).
+//                 (kinetic.py:148-224) from rows i-1, i, i+1 and writes g' and
+//                 the row moments <xi g'>, <g'^2>.  Only kinetic rows are
+//                 visited (compacted row list).
 //   cluster barrier
-//   slice phase   the leader CTA: masked rho update (hybrid.py:117-119,
-//                 kinetic.py:232-240, fluid.py:55-57), field solve
-//                 (poisson.py:21-54), J, remainder/perturbation indicators and
-//                 labels for the next step (adaptation.py:120-181), Chapman-
-//                 Enskog re-initialisation of flipped rows (lifting.py:38-105),
-//                 projection coefficients and the next kinetic-row list.
+//   slice phase   the leader CTA, on shared-memory copies of the slice
+//                 vectors: masked rho update (hybrid.py:117-119, kinetic.py:
+//                 232-240, fluid.py:55-57), field solve (poisson.py:21-54), J,
+//                 remainder/perturbation indicators and labels for the next
+//                 step (adaptation.py:120-181), Chapman-Enskog re-initialisation
+//                 of flipped rows (lifting.py:38-105), projection
+//                 coefficients and the next kinetic-row list.
 //   cluster barrier
 // g is double-buffered in HBM/L2 (the mixed update reads stale neighbours,
-// SURVEY F9).  Arithmetic follows numpy's operation order (Appendix A of
-// SURVEY.md) so results are bitwise equal to the reference.
+// SURVEY F9).  Arithmetic follows numpy's operation order
+// so results are bitwise equal to the reference.
 #include <cooperative_groups.h>
 
 #include "../../include/pk.h"
-#include "pk_args.h"
+#include "pk_rows.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace pk {
 
 // ---------------------------------------------------------------------------
-// Row layouts.  A warp owns one interface row g[i, 0..nv).
+// TMA bulk copy + mbarrier primitives.
 
-// Fast layout, nv = 64 P: lane l, slot s < P holds column 32 s + l (xi < 0),
-// slot T-1-s holds its mirror nv-1-(32 s + l) (xi > 0).  Mirror pairs sit in
-// one lane, so the velocity fold is register-local; loads stay coalesced.
-template <int T>
-struct Fast {
-  static constexpr int P = T / 2;
-  __device__ static __forceinline__ int col(int lane, int s) {
-    return s < P ? 32 * s + lane : 32 * s + 31 - lane;
-  }
-};
-
-template <int T>
-__device__ __forceinline__ void fast_load(double (&v)[T], const double* row, int lane) {
-#pragma unroll
-  for (int s = 0; s < T; ++s) v[s] = __ldcg(row + Fast<T>::col(lane, s));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-template <int T>
-__device__ __forceinline__ void fast_store(const double (&v)[T], double* row, int lane) {
-#pragma unroll
-  for (int s = 0; s < T; ++s) __stcg(row + Fast<T>::col(lane, s), v[s]);
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
 }
 
-// Folded velocity integral of q (mesh.py:95-133): mirror-pair fold, then
-// numpy's pairwise order (eight interleaved accumulators per block of <= 128
-// folded terms, xor-butterfly tree), times dv3.  Same bits on every lane.
-template <int T>
-__device__ __forceinline__ double fast_bracket(const double (&q)[T], int lane, double dv3) {
-  constexpr int P = T / 2;
-  double f[P];
-#pragma unroll
-  for (int t = 0; t < P; ++t) f[t] = q[t] + q[T - 1 - t];
-  const int k = lane & 7;
-  auto block = [&](int t0, int t1) {
-    double r = __shfl_sync(FULL, f[t0], k);
-#pragma unroll
-    for (int t = t0; t < t1; ++t) {
-#pragma unroll
-      for (int qq = (t == t0 ? 1 : 0); qq < 4; ++qq) r = r + __shfl_sync(FULL, f[t], k + 8 * qq);
-    }
-    r = r + __shfl_xor_sync(FULL, r, 1);
-    r = r + __shfl_xor_sync(FULL, r, 2);
-    r = r + __shfl_xor_sync(FULL, r, 4);
-    return r;
-  };
-  double tot;
-  if constexpr (P <= 4) {
-    tot = block(0, P);
-  } else {  // 256 folded terms: numpy splits at 128
-    const double a = block(0, 4);
-    const double b = block(4, 8);
-    tot = a + b;
-  }
-  return tot * dv3;
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)),
+               "r"(bytes)
+               : "memory");
 }
 
-// Per-lane velocity constants in slot order.
-template <int T>
-struct FastConsts {
-  double vx[T], M[T], xiM[T];
-  __device__ void load(const double* svx, const double* sM, const double* sxiM, int lane) {
-#pragma unroll
-    for (int s = 0; s < T; ++s) {
-      const int c = Fast<T>::col(lane, s);
-      vx[s] = svx[c];
-      M[s] = sM[c];
-      xiM[s] = sxiM[c];
-    }
-  }
-};
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(m))
+      : "memory");
+}
 
-struct RowCoef {
-  double vco, dc, J, k1, k2;
-  int vsg;
-};
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(m)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
 
-// One micro update of row i (kinetic.py:164-193,220-224 / hybrid.py:91-110).
-// gp, gc, gn: rows i-1, i, i+1 (as stored).  out: g'.
-template <int T>
-__device__ __forceinline__ void fast_micro(const double (&gp)[T], const double (&gc)[T],
-                                           const double (&gn)[T], double (&out)[T],
-                                           const FastConsts<T>& C, const RowCoef& rc,
-                                           double dx, double rdx, int lane) {
-  constexpr int P = T / 2;
-  // velocity-upwind neighbours, chosen by sign(E): zero inflow at +-v*
-  double nb[T];
-  if (rc.vsg > 0) {  // need g_{j-1}
-    double up[T], dn[T];
-#pragma unroll
-    for (int s = 0; s < T; ++s) {
-      if (s < P) up[s] = __shfl_sync(FULL, gc[s], (lane + 31) & 31);
-      else dn[s] = __shfl_sync(FULL, gc[s], (lane + 1) & 31);
-    }
-#pragma unroll
-    for (int s = 0; s < T; ++s) {
-      if (s < P) nb[s] = lane >= 1 ? up[s] : (s >= 1 ? up[s > 0 ? s - 1 : 0] : 0.0);
-      else nb[s] = lane <= 30 ? dn[s] : (s > P ? dn[s > P ? s - 1 : P] : gc[P - 1]);
-    }
-  } else if (rc.vsg < 0) {  // need g_{j+1}
-    double up[T], dn[T];
-#pragma unroll
-    for (int s = 0; s < T; ++s) {
-      if (s < P) dn[s] = __shfl_sync(FULL, gc[s], (lane + 1) & 31);
-      else up[s] = __shfl_sync(FULL, gc[s], (lane + 31) & 31);
-    }
-#pragma unroll
-    for (int s = 0; s < T; ++s) {
-      if (s < P) nb[s] = lane <= 30 ? dn[s] : (s + 1 < P ? dn[s + 1 < P ? s + 1 : 0] : gc[P]);
-      else nb[s] = lane >= 1 ? up[s] : (s + 1 < T ? up[s + 1 < T ? s + 1 : T - 1] : 0.0);
-    }
-  }
-#pragma unroll
-  for (int s = 0; s < T; ++s) {
-    const double g = gc[s];
-    // x-upwind by sign(xi): xi<0 uses (g_{i+1}-g_i), xi>0 uses (g_i-g_{i-1})
-    double o = (s < P) ? C.vx[s] * (gn[s] - g) : C.vx[s] * (g - gp[s]);
-    o = qdiv(o, dx, rdx);
-    if (rc.vsg > 0) o = o + (g - nb[s]) * rc.vco;
-    else if (rc.vsg < 0) o = o + (nb[s] - g) * rc.vco;
-    o = o - C.M[s] * rc.dc;
-    const double forcing = o + C.xiM[s] * rc.J;
-    out[s] = rc.k1 * g - rc.k2 * forcing;
-  }
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
-// Generic layout (any nv <= 256): lane l, slot s holds column 32 s + l.  The
-// fold and the pairwise sum go through a per-warp shared-memory row.
-constexpr int GT = 8;  // slots: nv <= 256
-
-__device__ __forceinline__ void gen_load(double (&v)[GT], const double* row, int lane, int nv) {
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int c = 32 * s + lane;
-    v[s] = c < nv ? __ldcg(row + c) : 0.0;
-  }
-}
-
-__device__ __forceinline__ void gen_store(const double (&v)[GT], double* row, int lane, int nv) {
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int c = 32 * s + lane;
-    if (c < nv) __stcg(row + c, v[s]);
-  }
-}
-
-__device__ __forceinline__ double gen_bracket(const double (&q)[GT], double* wrow, int lane,
-                                              int nv, double dv3) {
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int c = 32 * s + lane;
-    if (c < nv) wrow[c] = q[s];
-  }
-  __syncwarp();
-  const int h = nv / 2;
-  double mid = (nv & 1) ? wrow[h] : 0.0;
-  double f[GT];
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int j = 32 * s + lane;
-    f[s] = j < h ? wrow[j] + wrow[nv - 1 - j] : 0.0;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int j = 32 * s + lane;
-    if (j < h) wrow[j] = f[s];
-  }
-  __syncwarp();
-  double tot = warp_leaf([&](int j) { return wrow[j]; }, 0, h, lane);
-  if (nv & 1) tot = tot + mid;
-  __syncwarp();
-  return tot * dv3;
-}
-
-__device__ __forceinline__ void gen_micro(const double (&gp)[GT], const double (&gc)[GT],
-                                          const double (&gn)[GT], double (&out)[GT],
-                                          const double* svx, const double* sM, const double* sxiM,
-                                          const RowCoef& rc, int nv, double dx, double rdx,
-                                          int lane) {
-  double left[GT], right[GT];
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const double u = __shfl_sync(FULL, gc[s], (lane + 31) & 31);
-    const double d = __shfl_sync(FULL, gc[s], (lane + 1) & 31);
-    left[s] = u;
-    right[s] = d;
-  }
-  double lfix[GT], rfix[GT];
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int c = 32 * s + lane;
-    // column c-1 for lane 0 is lane 31 of slot s-1; column c+1 for lane 31 is lane 0 of slot s+1
-    lfix[s] = lane >= 1 ? left[s] : (s >= 1 ? left[s >= 1 ? s - 1 : 0] : 0.0);
-    rfix[s] = lane <= 30 ? right[s] : (s + 1 < GT ? right[s + 1 < GT ? s + 1 : 0] : 0.0);
-    if (c == 0) lfix[s] = 0.0;
-    if (c + 1 >= nv) rfix[s] = 0.0;
-  }
-  const double Ep = rc.vsg > 0 ? rc.vco : 0.0;
-  const double Em = rc.vsg < 0 ? rc.vco : 0.0;
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int c = 32 * s + lane;
-    if (c >= nv) {
-      out[s] = 0.0;
-      continue;
-    }
-    const double xi = svx[c];
-    const double xp = xi > 0.0 ? xi : 0.0;
-    const double xm = xi < 0.0 ? xi : 0.0;
-    const double g = gc[s];
-    double o = xp * (g - gp[s]);
-    o = o + xm * (gn[s] - g);
-    o = qdiv(o, dx, rdx);
-    // literal reference terms (both signs) for the generic path
-    const double dm = (c == 0) ? g : g - lfix[s];
-    o = o + dm * Ep;
-    const double dp = (c == nv - 1) ? -g : rfix[s] - g;
-    o = o + dp * Em;
-    o = o - sM[c] * rc.dc;
-    const double forcing = o + sxiM[c] * rc.J;
-    out[s] = rc.k1 * g - rc.k2 * forcing;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Shared memory layout of a CTA.
-struct Smem {
-  double* vx;
-  double* M;
-  double* xiM;
-  double* w2;
-  PwPlan* plan;
-  double* red;    // pairwise scratch (MAX_LEAF + MAX_NODE)
-  double* wrow;   // generic rows: one nv-row per warp
-  int* misc;      // small ints
-};
-
-// Per-slice view of the workspace.
+// Per-slice view.  "Local" vectors belong to the leader CTA's slice phase and
+// live in shared memory when they fit (else in the global workspace);
+// "shared" vectors are exchanged between the CTAs of the cluster through L2.
 struct SliceView {
   int b, nx, nv;
-  double *rho, *E, *Eprev, *J, *fl, *sq, *bm, *dco, *vco, *tA, *tB, *tC, *tD, *tE, *blift;
-  int8_t* vsg;
+  // leader-local
+  double *rho, *E, *Eprev, *J, *tA, *tB, *tC, *tD, *tE, *bm, *blift;
   uint8_t *kc, *ki, *flip, *nza, *nzb, *kcn, *kin;
+  // cluster-shared (global)
+  double *gJ, *dco, *vco;
+  // row moments <xi g>, <g^2>: written by every warp of the cluster (fl_w /
+  // sq_w: the leader's shared memory through DSMEM, or global), read by the
+  // leader (fl / sq)
+  double *fl, *sq, *fl_w, *sq_w;
+  int8_t* vsg;
   int* klist;
   int* nk;
   int* abort_;
@@ -281,23 +98,86 @@ struct SliceView {
   double rb;
 };
 
-__device__ __forceinline__ SliceView make_view(const FineArgs& a, int b) {
-  SliceView v;
+// number of leader-local double / byte vectors (all-kinetic mode needs the
+// first NLOC_DK / NLOC_BK only)
+constexpr int NLOC_D = 13;
+constexpr int NLOC_B = 7;
+constexpr int NLOC_DK = 7;
+constexpr int NLOC_BK = 2;
+
+__device__ __forceinline__ void bind_shared(SliceView& v, const FineArgs& a, int b) {
   const int nx = a.m.nx;
   const size_t o = (size_t)b * nx;
   v.b = b;
   v.nx = nx;
   v.nv = a.m.nv;
-  v.rho = a.rho + o; v.E = a.E + o; v.Eprev = a.Eprev + o; v.J = a.J + o; v.fl = a.fl + o;
-  v.sq = a.sq + o; v.bm = a.bm + o; v.dco = a.dco + o; v.vco = a.vco + o; v.tA = a.tA + o;
-  v.tB = a.tB + o; v.tC = a.tC + o; v.tD = a.tD + o; v.tE = a.tE + o; v.blift = a.blift + o;
-  v.vsg = a.vsg + o; v.kc = a.kc + o; v.ki = a.ki + o; v.flip = a.flip + o; v.nza = a.nza + o;
-  v.nzb = a.nzb + o; v.kcn = a.kcn + o; v.kin = a.kin + o; v.klist = a.klist + o;
-  v.nk = a.nk + b; v.abort_ = a.abort_ + b;
+  v.gJ = a.J + o;
+  v.dco = a.dco + o;
+  v.vco = a.vco + o;
+  v.vsg = a.vsg + o;
+  v.klist = a.klist + o;
+  v.nk = a.nk + b;
+  v.abort_ = a.abort_ + b;
   v.ga = a.ga + o * a.m.nv;
   v.gb = a.gb + o * a.m.nv;
   v.rb = a.rho_bar[b];
-  return v;
+}
+
+// Leader-local vectors either in shared memory (loc != null: the same smem
+// offset in every CTA of the cluster) or global.  In the shared-memory
+// layout the micro phase writes the row moments straight into the leader's
+// shared memory through DSMEM.
+__device__ __forceinline__ void bind_local(SliceView& v, const FineArgs& a, int b, double* loc,
+                                           bool leader) {
+  const int nx = a.m.nx;
+  const size_t o = (size_t)b * nx;
+  if (loc) {
+    const int nd = a.adaptation ? NLOC_D : NLOC_DK;
+    const int nb = a.adaptation ? NLOC_B : NLOC_BK;
+    double* p = loc;
+    double* fl = nullptr;
+    double* sq = nullptr;
+    double** d[NLOC_D] = {&v.rho, &v.E, &v.Eprev, &v.J, &fl, &v.tA, &v.tB,
+                          &sq, &v.tC, &v.tD, &v.tE, &v.bm, &v.blift};
+    for (int k = 0; k < NLOC_D; ++k) *d[k] = k < nd ? p + (size_t)k * nx : nullptr;
+    uint8_t* q = reinterpret_cast<uint8_t*>(p + (size_t)nd * nx);
+    uint8_t** e[NLOC_B] = {&v.kc, &v.ki, &v.flip, &v.nza, &v.nzb, &v.kcn, &v.kin};
+    for (int k = 0; k < NLOC_B; ++k) *e[k] = k < nb ? q + (size_t)k * nx : nullptr;
+    if (!a.adaptation) {  // unused in all-kinetic mode: sq and nz flags in global
+      v.nza = a.nza + o;
+      v.nzb = a.nzb + o;
+      sq = a.sq + o;
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    v.fl = fl;
+    v.sq = sq;
+    v.fl_w = cl.map_shared_rank(fl, 0);
+    v.sq_w = a.adaptation ? cl.map_shared_rank(sq, 0) : sq;
+    if (!leader) {
+      v.rho = v.E = v.Eprev = v.J = v.tA = v.tB = v.tC = v.tD = v.tE = v.bm = v.blift = nullptr;
+    }
+  } else {
+    v.fl = v.fl_w = a.fl + o;
+    v.sq = v.sq_w = a.sq + o;
+    v.rho = a.rho + o;
+    v.E = a.E + o;
+    v.Eprev = a.Eprev + o;
+    v.J = a.lJ + o;
+    v.tA = a.tA + o;
+    v.tB = a.tB + o;
+    v.tC = a.tC + o;
+    v.tD = a.tD + o;
+    v.tE = a.tE + o;
+    v.bm = a.bm + o;
+    v.blift = a.blift + o;
+    v.kc = a.kc + o;
+    v.ki = a.ki + o;
+    v.flip = a.flip + o;
+    v.nza = a.nza + o;
+    v.nzb = a.nzb + o;
+    v.kcn = a.kcn + o;
+    v.kin = a.kin + o;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -310,29 +190,73 @@ __device__ __forceinline__ double stencil_at(const double* v, int i, int nx, con
 #pragma unroll
   for (int o = 0; o < 7; ++o) {
     const double c = m.stc[p - 1][o];
-    if (c != 0.0) acc = acc + c * __ldcg(v + wrap(i + o - 3, nx));
+    if (c != 0.0) acc = acc + c * v[wrap(i + o - 3, nx)];
   }
   return acc * m.sts[p - 1];
 }
 
-// E = solve_field(rho) into E_out; returns false on a solvability violation.
+// Two pairwise sums over the same plan in one sweep (defect and scale of
+// poisson.py:42-43).
+template <class F1, class F2>
+__device__ void block_pairwise2(F1 x1, F2 x2, const PwPlan& P, double* scratch, double& r1,
+                                double& r2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarp = blockDim.x >> 5;
+  const int W = P.nleaf + P.nnode;
+  for (int l = warp; l < P.nleaf; l += nwarp) {
+    const double v1 = warp_leaf(x1, P.leaf_off[l], P.leaf_len[l], lane);
+    const double v2 = warp_leaf(x2, P.leaf_off[l], P.leaf_len[l], lane);
+    if (lane == 0) {
+      scratch[l] = v1;
+      scratch[W + l] = v2;
+    }
+  }
+  __syncthreads();
+  int start = 0;
+  for (int lev = 0; lev < P.nlevel; ++lev) {
+    const int end = P.level_end[lev];
+    for (int j = start + threadIdx.x; j < end; j += blockDim.x) {
+      scratch[P.nleaf + j] = scratch[P.node_a[j]] + scratch[P.node_b[j]];
+      scratch[W + P.nleaf + j] = scratch[W + P.node_a[j]] + scratch[W + P.node_b[j]];
+    }
+    __syncthreads();
+    start = end;
+  }
+  const int root = P.nnode == 0 ? 0 : P.nleaf + P.nnode - 1;
+  r1 = scratch[root];
+  r2 = scratch[W + root];
+  __syncthreads();
+}
+
+// E_out = solve_field(rho); false on a solvability violation.
 // poisson.py:41-54: src=(rho-rb)dx; defect=sum(src); guard; src-=defect/nx;
 // E=cumsum(src); E-=mean(E).
 __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, double* src,
-                            double* E_out, double rtol, int exact_scan, const Smem& sm) {
+                            double* E_out, double rtol, int exact_scan, const Smem& sm,
+                            long long* dbg = nullptr) {
   const int nx = m.nx;
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = (__ldcg(rho + i) - rb) * m.dx;
+  long long c0 = dbg ? clock64() : 0;
+#define PK_TICK(k)                         \
+  if (dbg && threadIdx.x == 0) {           \
+    const long long c1 = clock64();        \
+    dbg[k] += c1 - c0;                     \
+    c0 = c1;                               \
+  }
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = (rho[i] - rb) * m.dx;
   __syncthreads();
-  const double defect = block_pairwise([&](int i) { return src[i]; }, *sm.plan, sm.red);
-  const double scale =
-      block_pairwise([&](int i) { return fabs(__ldcg(rho + i)); }, *sm.plan, sm.red) * m.dx;
-  // `abs(defect) > rtol * max(scale, tiny)`: a NaN defect compares False
-  // in Python too, so only a genuine violation raises.
-  const double lim = rtol * fmax(scale, 2.2250738585072014e-308);
-  if (fabs(defect) > lim) return false;
+  PK_TICK(0)
+  double defect, abssum;
+  block_pairwise2([&](int i) { return src[i]; }, [&](int i) { return fabs(rho[i]); }, *sm.plan,
+                  sm.red, defect, abssum);
+  PK_TICK(1)
+  const double scale = abssum * m.dx;
+  // `abs(defect) > rtol * max(scale, tiny)`: a NaN defect compares False in
+  // Python too, so only a genuine violation raises.
+  if (fabs(defect) > rtol * fmax(scale, 2.2250738585072014e-308)) return false;
   const double corr = defect / (double)nx;
   for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = src[i] - corr;
   __syncthreads();
+  PK_TICK(2)
   if (exact_scan) {
     warp_cumsum([&](int i) { return src[i]; }, [&](int i, double v) { E_out[i] = v; }, nx);
   } else {
@@ -340,10 +264,13 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
                     sm.red);
   }
   __syncthreads();
-  const double mean =
-      block_pairwise([&](int i) { return __ldcg(E_out + i); }, *sm.plan, sm.red) / (double)nx;
+  PK_TICK(3)
+  const double mean = block_pairwise([&](int i) { return E_out[i]; }, *sm.plan, sm.red) / (double)nx;
+  PK_TICK(4)
   for (int i = threadIdx.x; i < nx; i += blockDim.x) E_out[i] = E_out[i] - mean;
   __syncthreads();
+  PK_TICK(5)
+#undef PK_TICK
   return true;
 }
 
@@ -380,146 +307,10 @@ __device__ int block_excl_scan(int v, int* out_prefix, int* sbuf) {
 }
 
 // ---------------------------------------------------------------------------
-// Row-level helpers (warp per row) used by the slice phase and the prologue.
-
-struct LiftRow {
-  double negJ;   // (-eps_i) * J_i
-  double e2;     // eps_i ** 2
-  double drift;  // dJ_i - E_i J_i       (order 2)
-  double Rif;    // R at the interface   (higher_order)
-};
-
-// lifting.py:63-105 for one row: g = xi M (-eps J) [+ (eps^2 w) drift]
-// [+ (eps^2 M) R_if]; two zero-mass projections.  Returns <xi g> and <g^2>
-// via bx/bsq.
-template <int T>
-__device__ void fast_lift_row(double (&g)[T], const LiftRow& L, int order, int higher, int project,
-                              const Smem& sm, const MeshDev& m, int lane) {
-#pragma unroll
-  for (int s = 0; s < T; ++s) {
-    const int c = Fast<T>::col(lane, s);
-    double v = sm.xiM[c] * L.negJ;
-    if (order >= 2) {
-      v = v + (L.e2 * sm.w2[c]) * L.drift;
-      if (higher) v = v + (L.e2 * sm.M[c]) * L.Rif;
-    }
-    g[s] = v;
-  }
-  if (project) {
-    for (int pass = 0; pass < 2; ++pass) {
-      const double bb = fast_bracket<T>(g, lane, m.dv3) / m.m0;
-#pragma unroll
-      for (int s = 0; s < T; ++s) g[s] = g[s] - bb * sm.M[Fast<T>::col(lane, s)];
-    }
-  }
-}
-
-__device__ void gen_lift_row(double (&g)[GT], const LiftRow& L, int order, int higher, int project,
-                             const Smem& sm, const MeshDev& m, double* wrow, int lane) {
-  const int nv = m.nv;
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int c = 32 * s + lane;
-    if (c >= nv) {
-      g[s] = 0.0;
-      continue;
-    }
-    double v = sm.xiM[c] * L.negJ;
-    if (order >= 2) {
-      v = v + (L.e2 * sm.w2[c]) * L.drift;
-      if (higher) v = v + (L.e2 * sm.M[c]) * L.Rif;
-    }
-    g[s] = v;
-  }
-  if (project) {
-    for (int pass = 0; pass < 2; ++pass) {
-      const double bb = gen_bracket(g, wrow, lane, nv, m.dv3) / m.m0;
-#pragma unroll
-      for (int s = 0; s < GT; ++s) {
-        const int c = 32 * s + lane;
-        if (c < nv) g[s] = g[s] - bb * sm.M[c];
-      }
-    }
-  }
-}
-
-// Row moments <xi g>, <g^2>.
-template <int T>
-__device__ __forceinline__ void fast_moments(const double (&g)[T], const Smem& sm, double dv3,
-                                             int lane, double& bx, double& bsq) {
-  double q[T], r[T];
-#pragma unroll
-  for (int s = 0; s < T; ++s) {
-    q[s] = sm.vx[Fast<T>::col(lane, s)] * g[s];
-    r[s] = g[s] * g[s];
-  }
-  bx = fast_bracket<T>(q, lane, dv3);
-  bsq = fast_bracket<T>(r, lane, dv3);
-}
-
-__device__ __forceinline__ void gen_moments(const double (&g)[GT], const Smem& sm, int nv,
-                                            double dv3, double* wrow, int lane, double& bx,
-                                            double& bsq) {
-  double q[GT], r[GT];
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int c = 32 * s + lane;
-    q[s] = c < nv ? sm.vx[c] * g[s] : 0.0;
-    r[s] = g[s] * g[s];
-  }
-  bx = gen_bracket(q, wrow, lane, nv, dv3);
-  bsq = gen_bracket(r, wrow, lane, nv, dv3);
-}
-
-// Layout dispatch: T == 0 selects the generic layout.
-template <int T>
-struct Layout {
-  static constexpr int S = T == 0 ? GT : T;
-};
-
-template <int T>
-__device__ __forceinline__ void row_load(double (&v)[Layout<T>::S], const double* row, int lane,
-                                         int nv) {
-  if constexpr (T == 0) gen_load(v, row, lane, nv);
-  else fast_load<T>(v, row, lane);
-}
-
-template <int T>
-__device__ __forceinline__ void row_store(const double (&v)[Layout<T>::S], double* row, int lane,
-                                          int nv) {
-  if constexpr (T == 0) gen_store(v, row, lane, nv);
-  else fast_store<T>(v, row, lane);
-}
-
-template <int T>
-__device__ __forceinline__ void row_zero_store(double* row, int lane, int nv) {
-  double z[Layout<T>::S];
-#pragma unroll
-  for (int s = 0; s < Layout<T>::S; ++s) z[s] = 0.0;
-  row_store<T>(z, row, lane, nv);
-}
-
-template <int T>
-__device__ __forceinline__ void row_moments(const double (&g)[Layout<T>::S], const Smem& sm,
-                                            const MeshDev& m, double* wrow, int lane, double& bx,
-                                            double& bsq) {
-  if constexpr (T == 0) gen_moments(g, sm, m.nv, m.dv3, wrow, lane, bx, bsq);
-  else fast_moments<T>(g, sm, m.dv3, lane, bx, bsq);
-}
-
-template <int T>
-__device__ __forceinline__ void row_lift(double (&g)[Layout<T>::S], const LiftRow& L, int order,
-                                         int higher, int project, const Smem& sm,
-                                         const MeshDev& m, double* wrow, int lane) {
-  if constexpr (T == 0) gen_lift_row(g, L, order, higher, project, sm, m, wrow, lane);
-  else fast_lift_row<T>(g, L, order, higher, project, sm, m, lane);
-}
-
-// ---------------------------------------------------------------------------
-// Slice phase: prepare step `s` (labels, flips, projection coefficients,
-// row list).  `moment_all`: the fl/sq moments are valid on every row
+// Slice phase: prepare step `s` (labels, flips, projection coefficients, row
+// list) from rho, E (start of step s), Eprev and the moments fl/sq of the
+// rows stored in gin.  `moment_all`: moments are valid on every row
 // (prologue: user g) rather than only on the previous step's kinetic rows.
-// gin: the input buffer of step s; gout: its output buffer.
 template <int T>
 __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& sm, double dt,
                              int moment_all, double* gin, double* gout, uint8_t* nzin,
@@ -530,146 +321,152 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   int* sflags = sm.misc;  // [0]: any flip, [1..32]: scan scratch
 
-  // J from the (new) rho and E   (micro_step's fluid_flux, kinetic.py:221)
+  if (!a.adaptation) {
+    // all-kinetic: J, and the projection/E-upwind coefficients from the
+    // unmasked moments (kinetic.py:177-178,190-191,221)
+    for (int i = tid; i < nx; i += nt) {
+      const int in_ = wrap(i + 1, nx), ip = wrap(i - 1, nx);
+      v.kc[i] = 1;  // adaptation off: all kinetic (hybrid.py:167-168)
+      v.ki[i] = 1;
+      const double e = v.E[i];
+      const double J = flux_J(v.rho[i], v.rho[in_], e, m.dx);
+      v.J[i] = J;
+      v.gJ[i] = J;
+      v.dco[i] = (v.fl[in_] - v.fl[ip]) / m.two_dx;
+      v.vsg[i] = e > 0.0 ? 1 : (e < 0.0 ? -1 : 0);
+      v.vco[i] = e / m.dvx;
+    }
+    if (tid == 0) *v.nk = nx;
+    __syncthreads();
+    return true;
+  }
+
   for (int i = tid; i < nx; i += nt) {
-    const int in_ = wrap(i + 1, nx);
-    v.J[i] = flux_J(__ldcg(v.rho + i), __ldcg(v.rho + in_), __ldcg(v.E + i), m.dx);
+    const double J = flux_J(v.rho[i], v.rho[wrap(i + 1, nx)], v.E[i], m.dx);
+    v.J[i] = J;
+    v.gJ[i] = J;
   }
   if (tid == 0) sflags[0] = 0;
   __syncthreads();
-
-  if (a.adaptation) {
-    // remainder indicator (adaptation.py:120-152) at cells
-    for (int i = tid; i < nx; i += nt) {
-      const int ip = wrap(i - 1, nx);
-      v.tA[i] = (__ldcg(v.E + i) - __ldcg(v.Eprev + i)) / dt;      // (E - E_prev)/dt
-      v.tB[i] = 0.5 * (__ldcg(v.J + ip) + __ldcg(v.J + i));        // J_c
-    }
-    __syncthreads();
-    const double three_rb = 3.0 * v.rb;
-    for (int i = tid; i < nx; i += nt) {
-      const int ip = wrap(i - 1, nx);
-      const double dtEc = 0.5 * (__ldcg(v.tA + ip) + __ldcg(v.tA + i));
-      const double Ec = 0.5 * (__ldcg(v.E + ip) + __ldcg(v.E + i));
-      const double d1J = stencil_at(v.tB, i, nx, m, 1);
-      const double d2J = stencil_at(v.tB, i, nx, m, 2);
-      const double d3J = stencil_at(v.tB, i, nx, m, 3);
-      const double d1r = stencil_at(v.rho, i, nx, m, 1);
-      const double rho = __ldcg(v.rho + i);
-      const double Jc = __ldcg(v.tB + i);
-      const double R = -d3J + Ec * d2J + (2.0 * rho - three_rb) * d1J + 2.0 * Jc * d1r - d1r * dtEc;
-      v.tC[i] = R;    // unscaled R (lift, higher_order)
-      v.tD[i] = d1J;  // D1(J_c) (lift drift)
-      const double Rs = a.rscale ? a.rscale[(size_t)v.b * nx + i] * R : R;
-      // perturbation indicator (adaptation.py:155-159) on the incoming g
-      const double sqp = (moment_all || v.ki[ip]) ? __ldcg(v.sq + ip) : 0.0;
-      const double sqi = (moment_all || v.ki[i]) ? __ldcg(v.sq + i) : 0.0;
-      const double gn = sqrt(0.5 * (sqp + sqi));
-      const bool fR = fabs(Rs) < a.delta0;
-      const bool fg = gn < a.eta0;
-      const bool fluid = a.combine_and ? (fR && fg) : (fR || fg);
-      v.kcn[i] = fluid ? 0 : 1;
-    }
-    __syncthreads();
-    int anyflip = 0;
-    for (int i = tid; i < nx; i += nt) {
-      const uint8_t kin = v.kcn[i] | v.kcn[wrap(i + 1, nx)];
-      v.kin[i] = kin;
-      const uint8_t f = (kin && !v.ki[i]) ? 1 : 0;
-      v.flip[i] = f;
-      anyflip |= f;
-    }
-    if (anyflip) atomicOr(&sflags[0], 1);
-    __syncthreads();
-    if (sflags[0]) {
-      if (a.reinit == 0) {
-        if (a.lift_order != 1 && a.lift_order != 2) {
-          if (tid == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
-          return false;
-        }
-        if (a.lift_order >= 2 && a.time_elim != 0 && a.time_elim != 1) {
-          if (tid == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
-          return false;
-        }
-        // lift scalars at the flipped interfaces (lifting.py:63-88); dE_dt = (E - E_prev)/dt
-        for (int i = tid; i < nx; i += nt) {
-          if (!v.flip[i]) continue;
-          const int in_ = wrap(i + 1, nx);
-          const double dJ = 0.5 * (__ldcg(v.tD + i) + __ldcg(v.tD + in_));
-          v.tE[i] = dJ - __ldcg(v.E + i) * __ldcg(v.J + i);      // drift
-          v.tA[i] = 0.5 * (__ldcg(v.tC + i) + __ldcg(v.tC + in_));  // R_if (tA no longer needed)
-        }
-        __syncthreads();
-        for (int i = warp; i < nx; i += nwarp) {
-          if (!v.flip[i]) continue;
-          LiftRow L;
-          const size_t o = (size_t)v.b * nx + i;
-          L.negJ = a.neg_eps[o] * __ldcg(v.J + i);
-          L.e2 = a.eps2[o];
-          L.drift = __ldcg(v.tE + i);
-          L.Rif = __ldcg(v.tA + i);
-          double g[Layout<T>::S];
-          row_lift<T>(g, L, a.lift_order, a.time_elim == 1, 1, sm, m, sm.wrow + warp * nv, lane);
-          row_store<T>(g, gin + (size_t)i * nv, lane, nv);
-          double bx, bsq;
-          row_moments<T>(g, sm, m, sm.wrow + warp * nv, lane, bx, bsq);
-          if (lane == 0) v.blift[i] = bx;
-        }
-      } else if (a.reinit == 1) {
-        for (int i = warp; i < nx; i += nwarp) {
-          if (!v.flip[i]) continue;
-          row_zero_store<T>(gin + (size_t)i * nv, lane, nv);
-          if (lane == 0) v.blift[i] = 0.0;
-        }
-      } else {
-        if (tid == 0) set_status(a.status, PK_ERR_BAD_REINIT, v.b, step);
+  // remainder indicator (adaptation.py:120-152) at cells
+  for (int i = tid; i < nx; i += nt) {
+    const int ip = wrap(i - 1, nx);
+    v.tA[i] = (v.E[i] - v.Eprev[i]) / dt;   // (E - E_prev)/dt
+    v.tB[i] = 0.5 * (v.J[ip] + v.J[i]);     // J_c
+  }
+  __syncthreads();
+  const double three_rb = 3.0 * v.rb;
+  for (int i = tid; i < nx; i += nt) {
+    const int ip = wrap(i - 1, nx);
+    const double dtEc = 0.5 * (v.tA[ip] + v.tA[i]);
+    const double Ec = 0.5 * (v.E[ip] + v.E[i]);
+    const double d1J = stencil_at(v.tB, i, nx, m, 1);
+    const double d2J = stencil_at(v.tB, i, nx, m, 2);
+    const double d3J = stencil_at(v.tB, i, nx, m, 3);
+    const double d1r = stencil_at(v.rho, i, nx, m, 1);
+    const double rho = v.rho[i];
+    const double Jc = v.tB[i];
+    const double R = -d3J + Ec * d2J + (2.0 * rho - three_rb) * d1J + 2.0 * Jc * d1r - d1r * dtEc;
+    v.tC[i] = R;    // unscaled R (lift, higher_order)
+    v.tD[i] = d1J;  // D1(J_c) (lift drift)
+    const double Rs = a.rscale ? a.rscale[(size_t)v.b * nx + i] * R : R;
+    // perturbation indicator (adaptation.py:155-159) on the incoming g
+    const double sqp = (moment_all || v.ki[ip]) ? v.sq[ip] : 0.0;
+    const double sqi = (moment_all || v.ki[i]) ? v.sq[i] : 0.0;
+    const double gn = sqrt(0.5 * (sqp + sqi));
+    const bool fR = fabs(Rs) < a.delta0;
+    const bool fg = gn < a.eta0;
+    const bool fluid = a.combine_and ? (fR && fg) : (fR || fg);
+    v.kcn[i] = fluid ? 0 : 1;
+  }
+  __syncthreads();
+  int anyflip = 0;
+  for (int i = tid; i < nx; i += nt) {
+    const uint8_t kin = v.kcn[i] | v.kcn[wrap(i + 1, nx)];
+    v.kin[i] = kin;
+    const uint8_t f = (kin && !v.ki[i]) ? 1 : 0;
+    v.flip[i] = f;
+    anyflip |= f;
+  }
+  if (anyflip) atomicOr(&sflags[0], 1);
+  __syncthreads();
+  if (sflags[0]) {
+    if (a.reinit == 0) {
+      if (a.lift_order != 1 && a.lift_order != 2) {
+        if (tid == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
         return false;
       }
-    }
-    __syncthreads();
-    // masked projection moment (hybrid.py:103-105) on the post-flip rows
-    for (int i = tid; i < nx; i += nt) {
-      const bool valid = moment_all || v.ki[i];
-      const double b = v.kin[i] ? (v.flip[i] ? __ldcg(v.blift + i) : (valid ? __ldcg(v.fl + i) : 0.0))
-                                : 0.0;
-      v.bm[i] = b;
-      if (!moment_all && v.flip[i]) nzin[i] = 1;
-    }
-    __syncthreads();
-    for (int i = tid; i < nx; i += nt) {
-      v.kc[i] = v.kcn[i];
-      v.ki[i] = v.kin[i];
-    }
-  } else {
-    for (int i = tid; i < nx; i += nt) {
-      v.bm[i] = __ldcg(v.fl + i);
-      v.kc[i] = 1;
-      v.ki[i] = 1;
+      if (a.lift_order >= 2 && a.time_elim != 0 && a.time_elim != 1) {
+        if (tid == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
+        return false;
+      }
+      // lift scalars at the flipped interfaces (lifting.py:63-88); dE_dt = (E - E_prev)/dt
+      for (int i = tid; i < nx; i += nt) {
+        if (!v.flip[i]) continue;
+        const int in_ = wrap(i + 1, nx);
+        const double dJ = 0.5 * (v.tD[i] + v.tD[in_]);
+        v.tE[i] = dJ - v.E[i] * v.J[i];          // drift
+        v.tA[i] = 0.5 * (v.tC[i] + v.tC[in_]);   // R_if
+      }
+      __syncthreads();
+      for (int i = warp; i < nx; i += nwarp) {
+        if (!v.flip[i]) continue;
+        LiftRow L;
+        const size_t o = (size_t)v.b * nx + i;
+        L.negJ = a.neg_eps[o] * v.J[i];
+        L.e2 = a.eps2[o];
+        L.drift = v.tE[i];
+        L.Rif = v.tA[i];
+        double g[Layout<T>::S];
+        row_lift<T>(g, L, a.lift_order, a.time_elim == 1, 1, sm, m, sm.wrow + warp * nv, lane);
+        row_store<T>(g, gin + (size_t)i * nv, lane, nv);
+        double bx, bsq;
+        row_moments<T>(g, sm, m, sm.wrow + warp * nv, lane, bx, bsq);
+        if (lane == 0) v.blift[i] = bx;
+      }
+    } else if (a.reinit == 1) {
+      for (int i = warp; i < nx; i += nwarp) {
+        if (!v.flip[i]) continue;
+        row_zero_store<T>(gin + (size_t)i * nv, lane, nv);
+        if (lane == 0) v.blift[i] = 0.0;
+      }
+    } else {
+      if (tid == 0) set_status(a.status, PK_ERR_BAD_REINIT, v.b, step);
+      return false;
     }
   }
   __syncthreads();
-  // projection coefficient dc (kinetic.py:190-191) and the E-upwind factor
-  // max(E,0)/dvx or min(E,0)/dvx (kinetic.py:177-178)
-  int cnt = 0;
-  const int per = (nx + nt - 1) / nt;
-  const int lo = min(nx, tid * per), hi = min(nx, lo + per);
+  // masked projection moment (hybrid.py:103-105) on the post-flip rows
   for (int i = tid; i < nx; i += nt) {
-    const double bn = __ldcg(v.bm + wrap(i + 1, nx));
-    const double bp = __ldcg(v.bm + wrap(i - 1, nx));
-    v.dco[i] = (bn - bp) / m.two_dx;
-    const double e = __ldcg(v.E + i);
+    const bool valid = moment_all || v.ki[i];
+    v.bm[i] = v.kin[i] ? (v.flip[i] ? v.blift[i] : (valid ? v.fl[i] : 0.0)) : 0.0;
+    if (!moment_all && v.flip[i]) nzin[i] = 1;
+  }
+  __syncthreads();
+  for (int i = tid; i < nx; i += nt) {
+    v.kc[i] = v.kcn[i];
+    v.ki[i] = v.kin[i];
+  }
+  __syncthreads();
+  // projection coefficient dc (kinetic.py:190-191) and E-upwind factor
+  // max(E,0)/dvx or min(E,0)/dvx (kinetic.py:177-178); zero the output rows of
+  // interfaces that are not kinetic this step but may hold data in the output
+  // buffer (kinetic->fluid transitions, hybrid.py:166)
+  for (int i = tid; i < nx; i += nt) {
+    v.dco[i] = (v.bm[wrap(i + 1, nx)] - v.bm[wrap(i - 1, nx)]) / m.two_dx;
+    const double e = v.E[i];
     v.vsg[i] = e > 0.0 ? 1 : (e < 0.0 ? -1 : 0);
     v.vco[i] = e / m.dvx;
-  }
-  // zero the output rows of interfaces that are not kinetic this step but may
-  // hold data in the output buffer (kinetic->fluid transitions, hybrid.py:166)
-  for (int i = warp; i < nx; i += nwarp) {
     if (!v.ki[i] && nzout[i]) {
-      row_zero_store<T>(gout + (size_t)i * nv, lane, nv);
-      if (lane == 0) nzout[i] = 0;
+      double* row = gout + (size_t)i * nv;
+      for (int j = 0; j < nv; ++j) row[j] = 0.0;
+      nzout[i] = 0;
     }
   }
   // compacted kinetic-row list (order preserving)
+  const int per = (nx + nt - 1) / nt;
+  const int lo = min(nx, tid * per), hi = min(nx, lo + per);
+  int cnt = 0;
   for (int i = lo; i < hi; ++i) cnt += v.ki[i] ? 1 : 0;
   int pre;
   const int total = block_excl_scan(cnt, &pre, sm.misc + 1);
@@ -682,8 +479,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
 
 // Slice phase after step s: masked rho update and field.  Returns false on a
 // solvability violation.  kc/ki are the labels the step ran with.
-__device__ bool finish_step(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
-                            int step) {
+__device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int ph, int step) {
   const MeshDev& m = a.m;
   const int nx = m.nx;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -692,42 +488,54 @@ __device__ bool finish_step(const FineArgs& a, const SliceView& v, const Smem& s
   const double cflu = P.cflu[v.b];
   for (int i = tid; i < nx; i += nt) {
     const int ip = wrap(i - 1, nx);
-    const double rho = __ldcg(v.rho + i);
+    const double rho = v.rho[i];
     double r;
     if (v.kc[i]) {
-      const double fi = v.ki[i] ? __ldcg(v.fl + i) : 0.0;
-      const double fp = v.ki[ip] ? __ldcg(v.fl + ip) : 0.0;
+      const double fi = v.ki[i] ? v.fl[i] : 0.0;
+      const double fp = v.ki[ip] ? v.fl[ip] : 0.0;
       const double ci = P.cmac[o + i], cp = P.cmac[o + ip];
       r = (ci == cp) ? rho - ci * (fi - fp) : rho - (ci * fi - cp * fp);
     } else {
-      r = rho + cflu * (__ldcg(v.J + i) - __ldcg(v.J + ip));
+      r = rho + cflu * (v.J[i] - v.J[ip]);
     }
     v.tA[i] = r;
   }
   __syncthreads();
-  for (int i = tid; i < nx; i += nt) v.rho[i] = v.tA[i];
-  __syncthreads();
-  if (!slice_field(m, v.rho, v.rb, v.tA, v.tB, a.rtol, a.exact_scan, sm)) {
+  // rho <- new density; the old E becomes E_prev (pointer rotation)
+  double* t = v.rho;
+  v.rho = v.tA;
+  v.tA = t;
+  t = v.Eprev;
+  v.Eprev = v.E;
+  v.E = t;
+  if (!slice_field(m, v.rho, v.rb, v.tB, v.E, a.rtol, a.exact_scan, sm,
+                   (a.prof && v.b == 0) ? a.prof + 8 : nullptr)) {
     if (tid == 0) set_status(a.status, PK_ERR_SOLVABILITY, v.b, step);
     return false;
   }
-  for (int i = tid; i < nx; i += nt) {
-    v.Eprev[i] = v.E[i];
-    v.E[i] = v.tB[i];
-  }
-  __syncthreads();
   return true;
 }
 
 // ---------------------------------------------------------------------------
-// Micro phase: this warp's share of the kinetic rows of one step.
-template <int T, int D>
-__device__ void micro_phase(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
-                            const double* gin, double* gout, int wg, int nwg) {
+// Micro phase, TMA path (fast layouts): this warp's share of the kinetic
+// rows.  The rows it needs (i-1, i, i+1 for each listed i, deduplicated;
+// the list is sorted so the unwrapped row sequence is increasing) form a
+// stream; stream position q lives in ring slot (qb+q) % S and completes phase
+// ((qb+q) / S) & 1 of that slot's mbarrier.  One lane issues the bulk
+// copies up to S-1 rows ahead of the consumer.
+struct RowStream {
+  int p_prod, e_next, e_end, hi_p, q_prod;  // producer
+  int hi_c, qhi_c;                          // consumer
+};
+
+template <int T, int S>
+__device__ void micro_phase_tma(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
+                                const double* gin, double* gout, int wg, int nwg, double* ring,
+                                uint64_t* mbar, uint32_t& qbase) {
   const MeshDev& m = a.m;
-  const int nx = m.nx, nv = m.nv;
+  const int nx = m.nx;
+  constexpr int NV = 32 * T;
   const int lane = threadIdx.x & 31;
-  constexpr int S = Layout<T>::S;
   const int nk = __ldcg(v.nk);
   const bool dense = nk == nx;
   const int p0 = (int)(((long long)wg * nk) / nwg);
@@ -735,58 +543,162 @@ __device__ void micro_phase(const FineArgs& a, const SliceView& v, const Smem& s
   if (p0 >= p1) return;
   const PhaseDev& P = a.ph[ph];
   const size_t o = (size_t)v.b * nx;
-  double* wrow = sm.wrow + (threadIdx.x >> 5) * nv;
-  FastConsts<T == 0 ? 2 : T> C;
-  if constexpr (T != 0) C.load(sm.vx, sm.M, sm.xiM, lane);
+  FastConsts<T> C;
+  C.load(sm.vx, sm.M, sm.xiM, lane);
   auto rowid = [&](int p) { return dense ? p : __ldcg(v.klist + p); };
 
-  double gp[S], gc[S], gn[S];
-  double pf[D][S];
-  // prime the prefetch ring with rows list(p)+1
-#pragma unroll
-  for (int d = 0; d < D; ++d)
-    if (p0 + d < p1) row_load<T>(pf[d], gin + (size_t)wrap(rowid(p0 + d) + 1, nx) * nv, lane, nv);
-  int last = -2;
-  for (int base = p0; base < p1; base += D) {
-#pragma unroll
-    for (int u = 0; u < D; ++u) {
-      const int p = base + u;
-      if (p < p1) {
-        const int i = rowid(p);
-        if (i == last + 1) {
-#pragma unroll
-          for (int s = 0; s < S; ++s) {
-            gp[s] = gc[s];
-            gc[s] = gn[s];
-          }
-        } else {
-          row_load<T>(gp, gin + (size_t)wrap(i - 1, nx) * nv, lane, nv);
-          row_load<T>(gc, gin + (size_t)i * nv, lane, nv);
-        }
-#pragma unroll
-        for (int s = 0; s < S; ++s) gn[s] = pf[u][s];
-        if (p + D < p1) row_load<T>(pf[u], gin + (size_t)wrap(rowid(p + D) + 1, nx) * nv, lane, nv);
-        RowCoef rc;
-        rc.vsg = __ldcg(v.vsg + i);
-        rc.vco = __ldcg(v.vco + i);
-        rc.dc = __ldcg(v.dco + i);
-        rc.J = __ldcg(v.J + i);
-        rc.k1 = P.k1[o + i];
-        rc.k2 = P.k2[o + i];
-        double out[S];
-        if constexpr (T == 0)
-          gen_micro(gp, gc, gn, out, sm.vx, sm.M, sm.xiM, rc, nv, m.dx, m.rdx, lane);
-        else
-          fast_micro<T>(gp, gc, gn, out, C, rc, m.dx, m.rdx, lane);
-        row_store<T>(out, gout + (size_t)i * nv, lane, nv);
-        double bx, bsq;
-        row_moments<T>(out, sm, m, wrow, lane, bx, bsq);
-        if (lane == 0) {
-          v.fl[i] = bx;
-          v.sq[i] = bsq;
-        }
-        last = i;
+  // the rows written by the previous step / slice phase are read below by TMA
+  // (async proxy)
+  if (lane == 0) fence_proxy_async_global();
+  __syncwarp();
+
+  RowStream st;
+  st.p_prod = p0;
+  st.e_next = 1;
+  st.e_end = 0;  // empty: fetch the first entry's range
+  st.hi_p = -3;
+  st.q_prod = 0;
+  st.hi_c = -3;
+  st.qhi_c = -1;
+  const uint32_t bytes = NV * 8;
+
+  auto pump = [&](int q_limit) {
+    while (st.q_prod < q_limit) {
+      if (st.e_next > st.e_end) {
+        if (st.p_prod >= p1) break;
+        const int i = rowid(st.p_prod++);
+        st.e_next = max(i - 1, st.hi_p + 1);
+        st.e_end = i + 1;
+        continue;
       }
+      if (lane == 0) {
+        const uint32_t Q = qbase + (uint32_t)st.q_prod;
+        const int slot = (int)(Q % S);
+        uint64_t* mb = mbar + slot;
+        // slot reuse: its previous contents were read into registers and
+        // consumed by this warp's arithmetic before this point (program
+        // order), so no proxy fence is needed here
+        mbar_expect_tx(mb, bytes);
+        bulk_g2s(ring + slot * NV, gin + (size_t)wrap(st.e_next, nx) * NV, bytes, mb);
+      }
+      st.hi_p = st.e_next;
+      ++st.e_next;
+      ++st.q_prod;
+    }
+  };
+  auto fetch = [&](double (&r)[T], int q) {
+    const uint32_t Q = qbase + (uint32_t)q;
+    const int slot = (int)(Q % S);
+    mbar_wait(mbar + slot, (Q / S) & 1);
+    const double* src = ring + slot * NV;
+#pragma unroll
+    for (int s = 0; s < T; ++s) r[s] = src[Fast<T>::col(lane, s)];
+  };
+
+  pump(S);
+  // per-row coefficients, 32 list entries at a time (one coalesced load per
+  // array, broadcast by shuffle)
+  double c_vco = 0, c_dco = 0, c_J = 0, c_k1 = 0, c_k2 = 0;
+  int c_vsg = 0, c_row = 0;
+  int cbase = p0 - 64;
+  double gp[T], gc[T], gn[T];
+  int prev_i = -5;
+  for (int p = p0; p < p1; ++p) {
+    if (p - cbase >= 32) {
+      cbase = p;
+      const int pl = p + lane;
+      if (pl < p1) {
+        const int r = rowid(pl);
+        c_row = r;
+        c_vco = __ldcg(v.vco + r);
+        c_dco = __ldcg(v.dco + r);
+        c_J = __ldcg(v.gJ + r);
+        c_vsg = __ldcg(v.vsg + r);
+        c_k1 = __ldg(P.k1 + o + r);
+        c_k2 = __ldg(P.k2 + o + r);
+      }
+    }
+    const int src = p - cbase;
+    const int i = __shfl_sync(FULL, c_row, src);
+    // stream positions of rows i-1, i, i+1
+    int q_im1;
+    if (i - 1 > st.hi_c) {
+      q_im1 = st.qhi_c + 1;
+      st.qhi_c += 3;
+    } else {
+      st.qhi_c += (i + 1) - st.hi_c;
+      q_im1 = st.qhi_c - 2;
+    }
+    st.hi_c = i + 1;
+    if (i == prev_i + 1) {
+#pragma unroll
+      for (int s = 0; s < T; ++s) {
+        gp[s] = gc[s];
+        gc[s] = gn[s];
+      }
+      fetch(gn, q_im1 + 2);
+    } else {
+      fetch(gp, q_im1);
+      fetch(gc, q_im1 + 1);
+      fetch(gn, q_im1 + 2);
+    }
+    RowCoef rc;
+    rc.vsg = __shfl_sync(FULL, c_vsg, src);
+    rc.vco = __shfl_sync(FULL, c_vco, src);
+    rc.dc = __shfl_sync(FULL, c_dco, src);
+    rc.J = __shfl_sync(FULL, c_J, src);
+    rc.k1 = __shfl_sync(FULL, c_k1, src);
+    rc.k2 = __shfl_sync(FULL, c_k2, src);
+    double out[T];
+    fast_micro<T>(gp, gc, gn, out, C, rc, m.dx, m.rdx, lane);
+    __syncwarp();
+    pump(q_im1 + 1 + S);  // positions < pos(i) are free (already consumed)
+    fast_store<T>(out, gout + (size_t)i * NV, lane);
+    double bx, bsq;
+    fast_moments<T>(out, sm, m.dv3, lane, bx, bsq);
+    if (lane == 0) {
+      v.fl_w[i] = bx;
+      v.sq_w[i] = bsq;
+    }
+    prev_i = i;
+  }
+  qbase += (uint32_t)st.q_prod;
+}
+
+// Micro phase, generic layout (any nv <= 256, no TMA): direct row loads.
+__device__ void micro_phase_gen(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
+                                const double* gin, double* gout, int wg, int nwg) {
+  const MeshDev& m = a.m;
+  const int nx = m.nx, nv = m.nv;
+  const int lane = threadIdx.x & 31;
+  const int nk = __ldcg(v.nk);
+  const bool dense = nk == nx;
+  const int p0 = (int)(((long long)wg * nk) / nwg);
+  const int p1 = (int)(((long long)(wg + 1) * nk) / nwg);
+  const PhaseDev& P = a.ph[ph];
+  const size_t o = (size_t)v.b * nx;
+  double* wrow = sm.wrow + (threadIdx.x >> 5) * nv;
+  for (int p = p0; p < p1; ++p) {
+    const int i = dense ? p : __ldcg(v.klist + p);
+    double gp[GT], gc[GT], gn[GT];
+    gen_load(gp, gin + (size_t)wrap(i - 1, nx) * nv, lane, nv);
+    gen_load(gc, gin + (size_t)i * nv, lane, nv);
+    gen_load(gn, gin + (size_t)wrap(i + 1, nx) * nv, lane, nv);
+    RowCoef rc;
+    rc.vsg = __ldcg(v.vsg + i);
+    rc.vco = __ldcg(v.vco + i);
+    rc.dc = __ldcg(v.dco + i);
+    rc.J = __ldcg(v.gJ + i);
+    rc.k1 = P.k1[o + i];
+    rc.k2 = P.k2[o + i];
+    double out[GT];
+    gen_micro(gp, gc, gn, out, sm.vx, sm.M, sm.xiM, rc, nv, m.dx, m.rdx, lane);
+    gen_store(out, gout + (size_t)i * nv, lane, nv);
+    double bx, bsq;
+    gen_moments(out, sm, nv, m.dv3, wrow, lane, bx, bsq);
+    if (lane == 0) {
+      v.fl_w[i] = bx;
+      v.sq_w[i] = bsq;
     }
   }
 }
@@ -795,7 +707,8 @@ __device__ void micro_phase(const FineArgs& a, const SliceView& v, const Smem& s
 // step-0 input buffer and compute their moments.
 template <int T>
 __device__ void prologue_rows(const FineArgs& a, const SliceView& v, const Smem& sm, double* gin0,
-                              bool lift, int wg, int nwg) {
+                              bool lift, const double* lJ, const double* ldrift,
+                              const double* lRif, int wg, int nwg) {
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
   const int lane = threadIdx.x & 31;
@@ -808,10 +721,10 @@ __device__ void prologue_rows(const FineArgs& a, const SliceView& v, const Smem&
     if (lift) {
       LiftRow L;
       const size_t o = (size_t)v.b * nx + i;
-      L.negJ = a.neg_eps[o] * __ldcg(v.J + i);
+      L.negJ = a.neg_eps[o] * __ldcg(lJ + i);
       L.e2 = a.eps2[o];
-      L.drift = __ldcg(v.tE + i);
-      L.Rif = __ldcg(v.tA + i);
+      L.drift = __ldcg(ldrift + i);
+      L.Rif = __ldcg(lRif + i);
       row_lift<T>(g, L, a.lift_order, a.time_elim == 1, 1, sm, m, wrow, lane);
       row_store<T>(g, gin0 + (size_t)i * nv, lane, nv);
     } else {
@@ -821,47 +734,53 @@ __device__ void prologue_rows(const FineArgs& a, const SliceView& v, const Smem&
     double bx, bsq;
     row_moments<T>(g, sm, m, wrow, lane, bx, bsq);
     if (lane == 0) {
-      v.fl[i] = bx;
-      v.sq[i] = bsq;
+      v.fl_w[i] = bx;
+      v.sq_w[i] = bsq;
     }
   }
 }
 
 // Window-start lift scalars (parareal.py:171-178: lift(rho_in, E) with
-// dE_dt = None, i.e. dtE_c = 0).
-__device__ bool lift_scalars(const FineArgs& a, const SliceView& v, const Smem& sm) {
+// dE_dt = None, i.e. dtE_c = 0), written to cluster-shared arrays (global)
+// for every CTA's prologue row pass.
+__device__ bool lift_scalars(const FineArgs& a, const SliceView& v, const Smem& sm, double* out_J,
+                             double* out_drift, double* out_Rif) {
   const MeshDev& m = a.m;
   const int nx = m.nx, tid = threadIdx.x, nt = blockDim.x;
   if (a.lift_order != 1 && a.lift_order != 2) return false;
   if (a.lift_order == 2 && a.time_elim != 0 && a.time_elim != 1) return false;
+  const bool higher = a.lift_order == 2 && a.time_elim == 1;
+  // temporaries: J_c in tA, D1(J_c) in tB (leader-local in every layout),
+  // R in the global scratch tC (once per window)
+  double* Jc = v.tA;
+  double* d1 = v.tB;
+  double* R = a.tC + (size_t)v.b * nx;
   for (int i = tid; i < nx; i += nt) {
     const int ip = wrap(i - 1, nx);
-    v.tB[i] = 0.5 * (__ldcg(v.J + ip) + __ldcg(v.J + i));  // J_c
+    Jc[i] = 0.5 * (v.J[ip] + v.J[i]);
   }
   __syncthreads();
   const double three_rb = 3.0 * v.rb;
   for (int i = tid; i < nx; i += nt) {
-    const double d1J = stencil_at(v.tB, i, nx, m, 1);
-    v.tD[i] = d1J;
-    if (a.lift_order == 2 && a.time_elim == 1) {
+    const double d1J = stencil_at(Jc, i, nx, m, 1);
+    d1[i] = d1J;
+    if (higher) {
       const int ip = wrap(i - 1, nx);
-      const double Ec = 0.5 * (__ldcg(v.E + ip) + __ldcg(v.E + i));
-      const double d2J = stencil_at(v.tB, i, nx, m, 2);
-      const double d3J = stencil_at(v.tB, i, nx, m, 3);
+      const double Ec = 0.5 * (v.E[ip] + v.E[i]);
+      const double d2J = stencil_at(Jc, i, nx, m, 2);
+      const double d3J = stencil_at(Jc, i, nx, m, 3);
       const double d1r = stencil_at(v.rho, i, nx, m, 1);
-      const double rho = __ldcg(v.rho + i);
-      const double Jc = __ldcg(v.tB + i);
       const double dtEc = 0.0;
-      v.tC[i] = -d3J + Ec * d2J + (2.0 * rho - three_rb) * d1J + 2.0 * Jc * d1r - d1r * dtEc;
+      R[i] = -d3J + Ec * d2J + (2.0 * v.rho[i] - three_rb) * d1J + 2.0 * Jc[i] * d1r - d1r * dtEc;
     }
   }
   __syncthreads();
   for (int i = tid; i < nx; i += nt) {
     const int in_ = wrap(i + 1, nx);
-    const double dJ = 0.5 * (__ldcg(v.tD + i) + __ldcg(v.tD + in_));
-    v.tE[i] = dJ - __ldcg(v.E + i) * __ldcg(v.J + i);
-    v.tA[i] = (a.lift_order == 2 && a.time_elim == 1) ? 0.5 * (__ldcg(v.tC + i) + __ldcg(v.tC + in_))
-                                                     : 0.0;
+    const double dJ = 0.5 * (d1[i] + d1[in_]);
+    out_J[i] = v.J[i];
+    out_drift[i] = dJ - v.E[i] * v.J[i];
+    out_Rif[i] = higher ? 0.5 * (R[i] + R[in_]) : 0.0;
   }
   __syncthreads();
   return true;
@@ -875,7 +794,7 @@ __device__ __forceinline__ void cluster_barrier(int C) {
   }
 }
 
-template <int T, int D>
+template <int T, int S>
 __global__ void __launch_bounds__(256, 2) fine_kernel(const FineArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const MeshDev& m = a.m;
@@ -889,19 +808,32 @@ __global__ void __launch_bounds__(256, 2) fine_kernel(const FineArgs a) {
   }
   const int b = blockIdx.x / C;
   const bool leader = crank == 0;
+  const int nwpc = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5;
   // shared memory carve-up
   Smem sm;
+  double* ring = nullptr;
+  uint64_t* mbar = nullptr;
+  double* sm_loc = nullptr;
   {
     unsigned char* p = smem_raw;
+    mbar = reinterpret_cast<uint64_t*>(p);
+    p += 64 * 8;
     sm.plan = reinterpret_cast<PwPlan*>(p);
     p += (sizeof(PwPlan) + 15) / 16 * 16;
     sm.vx = reinterpret_cast<double*>(p); p += nv * 8;
     sm.M = reinterpret_cast<double*>(p); p += nv * 8;
     sm.xiM = reinterpret_cast<double*>(p); p += nv * 8;
     sm.w2 = reinterpret_cast<double*>(p); p += nv * 8;
-    sm.red = reinterpret_cast<double*>(p); p += (MAX_LEAF + MAX_NODE) * 8;
-    sm.wrow = reinterpret_cast<double*>(p); p += (blockDim.x >> 5) * nv * 8;
-    sm.misc = reinterpret_cast<int*>(p);
+    sm.red = reinterpret_cast<double*>(p); p += 2 * (MAX_LEAF + MAX_NODE) * 8;
+    sm.misc = reinterpret_cast<int*>(p); p += 64 * 4;
+    sm.wrow = reinterpret_cast<double*>(p);
+    if (T == 0) p += (size_t)nwpc * nv * 8;  // generic-layout row scratch
+    if (T != 0) {
+      ring = reinterpret_cast<double*>(p);
+      p += (size_t)nwpc * S * nv * 8;
+    }
+    if (a.local_smem) sm_loc = reinterpret_cast<double*>(p);  // same offset in every CTA
   }
   {
     const int* src = reinterpret_cast<const int*>(m.plan_x);
@@ -913,58 +845,71 @@ __global__ void __launch_bounds__(256, 2) fine_kernel(const FineArgs a) {
       sm.xiM[j] = m.xiM[j];
       sm.w2[j] = m.w2[j];
     }
+    if (T != 0 && threadIdx.x < nwpc * S) mbar_init(mbar + threadIdx.x, 1);
+    if (T != 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (b >= a.B) return;  // never: grid is exactly B clusters
 
-  const SliceView v = make_view(a, b);
+  SliceView v;
+  bind_shared(v, a, b);
+  bind_local(v, a, b, sm_loc, leader);
   const int n0 = a.ph[0].nsteps[b], n1 = a.ph[1].nsteps[b];
   const int nst = n0 + n1;
-  const int nwpc = blockDim.x >> 5;
-  const int wg = crank * nwpc + (threadIdx.x >> 5);
+  const int wg = crank * nwpc + warp;
   const int nwg = C * nwpc;
   const int initf = a.init_flags ? a.init_flags[b] : 0;
-  const bool lift0 = (initf & 1) != 0;       // g := lift(rho, E)   (parareal.py:171-178)
-  const bool eprev0 = (initf & 2) != 0;      // E_prev := E         (hybrid.py:68-72)
+  const bool lift0 = (initf & 1) != 0;   // g := lift(rho, E)   (parareal.py:171-178)
+  const bool eprev0 = (initf & 2) != 0;  // E_prev := E         (hybrid.py:68-72)
   // step s reads buf(s) and writes buf(s+1); the last output lands in ga.
   auto buf = [&](int s) { return ((s + (nst & 1)) & 1) ? v.gb : v.ga; };
   auto nzf = [&](int s) { return ((s + (nst & 1)) & 1) ? v.nzb : v.nza; };
   int* abort_flag = v.abort_;
+  const size_t o = (size_t)b * nx;
+  uint32_t qbase = 0;
+  double* ring_w = ring ? ring + (size_t)warp * S * nv : nullptr;
+  uint64_t* mbar_w = mbar + warp * S;
 
   // ---- prologue ----
   if (leader) {
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < nx; i += nt) {
       v.nza[i] = 1;
       v.nzb[i] = 1;
+      if (sm_loc) {
+        v.rho[i] = a.rho[o + i];
+        v.Eprev[i] = a.Eprev[o + i];
+        v.kc[i] = a.kc[o + i];
+        v.ki[i] = a.ki[o + i];
+      }
     }
-    if (threadIdx.x == 0) *abort_flag = 0;
+    if (tid == 0) *abort_flag = 0;
+    __syncthreads();
     bool ok = slice_field(m, v.rho, v.rb, v.tA, v.E, a.rtol, a.exact_scan, sm);
     if (!ok) {
-      if (threadIdx.x == 0) {
+      if (tid == 0) {
         set_status(a.status, PK_ERR_SOLVABILITY, b, 0);
         *abort_flag = 1;
       }
     } else {
-      for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-        const int in_ = wrap(i + 1, nx);
-        v.J[i] = flux_J(__ldcg(v.rho + i), __ldcg(v.rho + in_), __ldcg(v.E + i), m.dx);
+      for (int i = tid; i < nx; i += nt) {
+        v.J[i] = flux_J(v.rho[i], v.rho[wrap(i + 1, nx)], v.E[i], m.dx);
+        if (eprev0) v.Eprev[i] = v.E[i];
       }
       __syncthreads();
-      if (lift0 && !lift_scalars(a, v, sm)) {
-        if (threadIdx.x == 0) {
+      // window-start lift scalars go to cluster-shared scratch (dco/vco/gJ
+      // are not in use before the first prepare_step)
+      if (lift0 && !lift_scalars(a, v, sm, v.gJ, v.dco, v.vco)) {
+        if (tid == 0) {
           set_status(a.status, PK_ERR_BAD_LIFT, b, 0);
           *abort_flag = 1;
         }
       }
     }
     __syncthreads();
-    if (eprev0 && !*abort_flag) {
-      for (int i = threadIdx.x; i < nx; i += blockDim.x) v.Eprev[i] = v.E[i];
-    }
   }
   cluster_barrier(C);
   if (__ldcg(abort_flag)) return;
-  prologue_rows<T>(a, v, sm, buf(0), lift0, wg, nwg);
+  prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, wg, nwg);
   cluster_barrier(C);
   if (leader) {
     const double dt0 = (n0 > 0 ? a.ph[0].dt : a.ph[1].dt)[b];
@@ -976,25 +921,63 @@ __global__ void __launch_bounds__(256, 2) fine_kernel(const FineArgs a) {
   if (__ldcg(abort_flag)) return;
 
   // ---- steps ----
+  // optional phase profile (slice 0, leader thread 0): clock64 deltas of
+  // [micro, barrier, finish, prepare, barrier]
+  const bool prof = a.prof && b == 0 && leader && threadIdx.x == 0;
+  long long tp[6] = {0, 0, 0, 0, 0, 0};
+  long long c0 = prof ? clock64() : 0, c1;
   for (int s = 0; s < nst; ++s) {
     const int ph = s < n0 ? 0 : 1;
-    micro_phase<T, D>(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
+    if constexpr (T != 0)
+      micro_phase_tma<T, S>(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg, ring_w, mbar_w, qbase);
+    else
+      micro_phase_gen(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
+    if (prof) { c1 = clock64(); tp[0] += c1 - c0; c0 = c1; }
     cluster_barrier(C);
+    if (prof) { c1 = clock64(); tp[1] += c1 - c0; c0 = c1; }
     if (leader) {
       bool ok = finish_step(a, v, sm, ph, s);
+      if (prof) { c1 = clock64(); tp[2] += c1 - c0; c0 = c1; }
       if (ok && s + 1 < nst) {
         // step s+1 reads buf(s+1) and writes buf(s+2) == buf(s); after step
         // s the rows of buf(s+1) hold data exactly on step s's kinetic rows.
-        uint8_t* nzn = nzf(s + 1);
-        for (int i = threadIdx.x; i < nx; i += blockDim.x) nzn[i] = v.ki[i];
-        __syncthreads();
+        if (a.adaptation) {
+          uint8_t* nzn = nzf(s + 1);
+          for (int i = threadIdx.x; i < nx; i += blockDim.x) nzn[i] = v.ki[i];
+          __syncthreads();
+        }
         const int phn = (s + 1) < n0 ? 0 : 1;
-        ok = prepare_step<T>(a, v, sm, a.ph[phn].dt[b], 0, buf(s + 1), buf(s), nzn, nzf(s), s + 1);
+        ok = prepare_step<T>(a, v, sm, a.ph[phn].dt[b], 0, buf(s + 1), buf(s), nzf(s + 1),
+                             nzf(s), s + 1);
       }
       if (!ok && threadIdx.x == 0) *abort_flag = 1;
+      if (prof) { c1 = clock64(); tp[3] += c1 - c0; c0 = c1; }
     }
     cluster_barrier(C);
+    if (prof) { c1 = clock64(); tp[4] += c1 - c0; c0 = c1; }
     if (__ldcg(abort_flag)) return;
+  }
+  if (prof) {
+    for (int k = 0; k < 5; ++k) a.prof[k] += tp[k];
+    a.prof[5] += nst;
+  }
+  // ---- epilogue: leader-local state back to the caller's arrays ----
+  if (leader && sm_loc) {
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      a.rho[o + i] = v.rho[i];
+      a.E[o + i] = v.E[i];
+      a.Eprev[o + i] = v.Eprev[i];
+      a.kc[o + i] = v.kc[i];
+      a.ki[o + i] = v.ki[i];
+    }
+  } else if (leader) {
+    // global mode: rho/E/Eprev rotate through rho/E/Eprev/tA/tB pointers
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      const double r = v.rho[i], e = v.E[i], ep = v.Eprev[i];
+      a.rho[o + i] = r;
+      a.E[o + i] = e;
+      a.Eprev[o + i] = ep;
+    }
   }
 }
 
@@ -1031,16 +1014,16 @@ __global__ void __launch_bounds__(256) lift_kernel(const LiftArgs a) {
   const double* E = a.E + o;
   double *J = a.J + o, *Jc = a.tA + o, *d1 = a.tB + o, *drift = a.tC + o, *R = a.tD + o,
          *Rif = a.tE + o;
-  for (int i = tid; i < nx; i += nt)
-    J[i] = flux_J(rho[i], rho[wrap(i + 1, nx)], E[i], m.dx);
+  for (int i = tid; i < nx; i += nt) J[i] = flux_J(rho[i], rho[wrap(i + 1, nx)], E[i], m.dx);
   __syncthreads();
   const bool higher = a.order >= 2 && a.time_elim == 1;
   if (a.order >= 2) {
-    for (int i = tid; i < nx; i += nt) Jc[i] = 0.5 * (__ldcg(J + wrap(i - 1, nx)) + __ldcg(J + i));
+    for (int i = tid; i < nx; i += nt) Jc[i] = 0.5 * (J[wrap(i - 1, nx)] + J[i]);
     __syncthreads();
     const double three_rb = 3.0 * a.rho_bar[b];
     for (int i = tid; i < nx; i += nt) {
-      d1[i] = stencil_at(Jc, i, nx, m, 1);
+      const double d1J = stencil_at(Jc, i, nx, m, 1);
+      d1[i] = d1J;
       if (higher) {
         const int ip = wrap(i - 1, nx);
         const double Ec = 0.5 * (E[ip] + E[i]);
@@ -1048,17 +1031,15 @@ __global__ void __launch_bounds__(256) lift_kernel(const LiftArgs a) {
         const double d2J = stencil_at(Jc, i, nx, m, 2);
         const double d3J = stencil_at(Jc, i, nx, m, 3);
         const double d1r = stencil_at(rho, i, nx, m, 1);
-        const double d1J = __ldcg(d1 + i);
-        R[i] = -d3J + Ec * d2J + (2.0 * rho[i] - three_rb) * d1J + 2.0 * __ldcg(Jc + i) * d1r -
-               d1r * dtEc;
+        R[i] = -d3J + Ec * d2J + (2.0 * rho[i] - three_rb) * d1J + 2.0 * Jc[i] * d1r - d1r * dtEc;
       }
     }
     __syncthreads();
     for (int i = tid; i < nx; i += nt) {
       const int in_ = wrap(i + 1, nx);
-      const double dJ = 0.5 * (__ldcg(d1 + i) + __ldcg(d1 + in_));
-      drift[i] = dJ - E[i] * __ldcg(J + i);
-      Rif[i] = higher ? 0.5 * (__ldcg(R + i) + __ldcg(R + in_)) : 0.0;
+      const double dJ = 0.5 * (d1[i] + d1[in_]);
+      drift[i] = dJ - E[i] * J[i];
+      Rif[i] = higher ? 0.5 * (R[i] + R[in_]) : 0.0;
     }
   }
   __syncthreads();
@@ -1066,10 +1047,10 @@ __global__ void __launch_bounds__(256) lift_kernel(const LiftArgs a) {
   double* wrow = sm.wrow + warp * nv;
   for (int i = warp; i < nx; i += nwarp) {
     LiftRow L;
-    L.negJ = a.neg_eps[o + i] * __ldcg(J + i);
+    L.negJ = a.neg_eps[o + i] * J[i];
     L.e2 = a.eps2[o + i];
-    L.drift = a.order >= 2 ? __ldcg(drift + i) : 0.0;
-    L.Rif = a.order >= 2 ? __ldcg(Rif + i) : 0.0;
+    L.drift = a.order >= 2 ? drift[i] : 0.0;
+    L.Rif = a.order >= 2 ? Rif[i] : 0.0;
     double g[Layout<T>::S];
     row_lift<T>(g, L, a.order, higher, a.project, sm, m, wrow, lane);
     row_store<T>(g, a.g_out + (o + i) * nv, lane, nv);
@@ -1097,16 +1078,32 @@ __global__ void __launch_bounds__(256) field_kernel(const FieldArgs a) {
 // ---------------------------------------------------------------------------
 // Host-side launch.
 
-size_t fine_smem_bytes(int nv, int threads) {
-  return (sizeof(PwPlan) + 15) / 16 * 16 + 4 * nv * 8 + (MAX_LEAF + MAX_NODE) * 8 +
-         (threads / 32) * nv * 8 + 64 * 4;
+constexpr int kThreads = 256;
+
+static size_t base_smem(int nv, int T, int S) {
+  size_t s = 64 * 8 + (sizeof(PwPlan) + 15) / 16 * 16 + 4 * (size_t)nv * 8 +
+             2 * (MAX_LEAF + MAX_NODE) * 8 + 64 * 4;
+  if (T == 0) s += (kThreads / 32) * (size_t)nv * 8;
+  else s += (size_t)(kThreads / 32) * S * nv * 8;
+  return s;
 }
 
-template <int T, int D>
-static cudaError_t launch_T(const FineArgs& a, int C, cudaStream_t st) {
-  const int threads = 256;
-  const size_t smem = fine_smem_bytes(a.m.nv, threads);
-  auto kern = fine_kernel<T, D>;
+static size_t local_smem(int nx, int adaptation) {
+  return adaptation ? (size_t)nx * (NLOC_D * 8 + NLOC_B) + 16
+                    : (size_t)nx * (NLOC_DK * 8 + NLOC_BK) + 16;
+}
+
+template <int T, int S>
+static cudaError_t launch_T(FineArgs a, int C, cudaStream_t st) {
+  const size_t base = base_smem(a.m.nv, T, S);
+  // slice vectors on chip when two CTAs still fit per SM
+  size_t smem = base;
+  a.local_smem = 0;
+  if (base + local_smem(a.m.nx, a.adaptation) <= 112 * 1024) {
+    a.local_smem = 1;
+    smem = base + local_smem(a.m.nx, a.adaptation);
+  }
+  auto kern = fine_kernel<T, S>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (C > 8) {
@@ -1115,7 +1112,7 @@ static cudaError_t launch_T(const FineArgs& a, int C, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.B * C);
-  cfg.blockDim = dim3(threads);
+  cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1130,12 +1127,11 @@ static cudaError_t launch_T(const FineArgs& a, int C, cudaStream_t st) {
 
 template <int T>
 static cudaError_t launch_lift_T(const LiftArgs& a, cudaStream_t st) {
-  const int threads = 256;
-  const size_t smem = 4 * a.m.nv * 8 + (threads / 32) * a.m.nv * 8;
+  const size_t smem = 4 * a.m.nv * 8 + (kThreads / 32) * a.m.nv * 8;
   cudaError_t e =
       cudaFuncSetAttribute(lift_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  lift_kernel<T><<<a.B, threads, smem, st>>>(a);
+  lift_kernel<T><<<a.B, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -1156,16 +1152,16 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
   cudaError_t e =
       cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  field_kernel<<<a.B, 256, smem, st>>>(a);
+  field_kernel<<<a.B, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   switch (a.m.nv) {
-    case 64: return launch_T<2, 4>(a, C, st);
-    case 128: return launch_T<4, 3>(a, C, st);
-    case 256: return launch_T<8, 2>(a, C, st);
-    case 512: return launch_T<16, 1>(a, C, st);
+    case 64: return launch_T<2, 6>(a, C, st);
+    case 128: return launch_T<4, 4>(a, C, st);
+    case 256: return launch_T<8, 3>(a, C, st);
+    case 512: return launch_T<16, 3>(a, C, st);
     default:
       if (a.m.nv <= 32 * GT) return launch_T<0, 1>(a, C, st);
       return cudaErrorInvalidValue;
