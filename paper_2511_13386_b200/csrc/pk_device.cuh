@@ -123,6 +123,50 @@ __device__ __forceinline__ void warp_cumsum(FS src, FD dst, int n) {
   }
 }
 
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+
+__device__ __forceinline__ void sts64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
+// warp_cumsum for operands that live in shared memory: explicit LDS/STS
+// (generic accesses cost ~2.5x the chain latency).  Thread 0 only.
+__device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int n) {
+  if (threadIdx.x != 0) return;
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(src);
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  constexpr int K = 16;
+  double acc = -0.0;
+  const int nk = n - n % K;
+  double cur[K];
+  if (nk > 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) cur[k] = lds64(s + 8 * k);
+  }
+  for (int i = 0; i < nk; i += K) {
+    double nxt[K];
+    if (i + K < nk) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) nxt[k] = lds64(s + 8 * (i + K + k));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      acc = acc + cur[k];
+      sts64(d + 8 * (i + k), acc);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) cur[k] = nxt[k];
+  }
+  for (int i = nk; i < n; ++i) {
+    acc = acc + lds64(s + 8 * i);
+    sts64(d + 8 * i, acc);
+  }
+}
+
 // Work-efficient parallel prefix sum (fast mode, not bitwise): block scan with
 // warp shuffles over a blocked partition.  `scratch` holds blockDim.x/32 + 1
 // doubles.  Result differs from np.cumsum by O(n u |E|).

@@ -258,7 +258,10 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
   __syncthreads();
   PK_TICK(2)
   if (exact_scan) {
-    warp_cumsum([&](int i) { return src[i]; }, [&](int i, double v) { E_out[i] = v; }, nx);
+    if (__isShared(src) && __isShared(E_out))
+      smem_cumsum(src, E_out, nx);
+    else
+      warp_cumsum([&](int i) { return src[i]; }, [&](int i, double v) { E_out[i] = v; }, nx);
   } else {
     block_scan_fast([&](int i) { return src[i]; }, [&](int i, double v) { E_out[i] = v; }, nx,
                     sm.red);
@@ -665,6 +668,208 @@ __device__ void micro_phase_tma(const FineArgs& a, const SliceView& v, const Sme
   qbase += (uint32_t)st.q_prod;
 }
 
+// Micro phase, G8 layout (nv = 16 CH: 64, 128): eight lanes own one row and
+// lane k owns the whole pairwise chain k of the velocity fold (columns
+// k + 8m and their mirrors nv-1-k-8m), so the bracket needs no cross-lane
+// traffic until the final 8-way tree; a warp advances four rows at a time.
+// Every operand (row i, its x-neighbours, the velocity neighbours) is read
+// from the TMA ring in shared memory; ring rows are padded by 64 B so the
+// four groups of a warp hit distinct bank halves.
+template <int CH, int S>
+__device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
+                               const double* gin, double* gout, int wg, int nwg, double* ring,
+                               uint64_t* mbar, uint32_t& qbase) {
+  constexpr int NV = 16 * CH;
+  constexpr int RS = NV + 8;  // ring row stride in doubles
+  const MeshDev& m = a.m;
+  const int nx = m.nx;
+  const int lane = threadIdx.x & 31;
+  const int k = lane & 7, gr = lane >> 3;
+  const int nk = __ldcg(v.nk);
+  const bool dense = nk == nx;
+  const int p0 = (int)(((long long)wg * nk) / nwg);
+  const int p1 = (int)(((long long)(wg + 1) * nk) / nwg);
+  if (p0 >= p1) return;
+  const PhaseDev& P = a.ph[ph];
+  const size_t o = (size_t)v.b * nx;
+  const uint32_t s_vx = smem_u32(sm.vx), s_M = smem_u32(sm.M), s_xiM = smem_u32(sm.xiM);
+  const uint32_t s_ring = smem_u32(ring);
+  const double dx = m.dx, rdx = m.rdx, dv3 = m.dv3;
+  auto rowid = [&](int p) { return dense ? p : __ldcg(v.klist + p); };
+
+  if (lane == 0) fence_proxy_async_global();  // rows written by the generic proxy, read by TMA
+  __syncwarp();
+
+  RowStream st;
+  st.p_prod = p0;
+  st.e_next = 1;
+  st.e_end = 0;
+  st.hi_p = -3;
+  st.q_prod = 0;
+  st.hi_c = -3;
+  st.qhi_c = -1;
+  constexpr uint32_t bytes = NV * 8;
+  auto pump = [&](int q_limit) {
+    while (st.q_prod < q_limit) {
+      if (st.e_next > st.e_end) {
+        if (st.p_prod >= p1) break;
+        const int i = rowid(st.p_prod++);
+        st.e_next = max(i - 1, st.hi_p + 1);
+        st.e_end = i + 1;
+        continue;
+      }
+      if (lane == 0) {
+        const uint32_t Q = qbase + (uint32_t)st.q_prod;
+        const int slot = (int)(Q % S);
+        mbar_expect_tx(mbar + slot, bytes);
+        bulk_g2s(ring + slot * RS, gin + (size_t)wrap(st.e_next, nx) * NV, bytes, mbar + slot);
+      }
+      st.hi_p = st.e_next;
+      ++st.e_next;
+      ++st.q_prod;
+    }
+  };
+  auto slot_addr = [&](int q) {
+    const uint32_t Q = qbase + (uint32_t)q;
+    const int slot = (int)(Q % S);
+    mbar_wait(mbar + slot, (Q / S) & 1);
+    return s_ring + (uint32_t)(slot * RS * 8);
+  };
+
+  pump(S);
+  double c_vco = 0, c_dco = 0, c_J = 0, c_k1 = 0, c_k2 = 0;
+  int c_vsg = 0, c_row = 0;
+  int cbase = p0 - 64;
+  for (int p = p0; p < p1;) {
+    if (p + 4 - cbase > 32) {
+      cbase = p;
+      const int pl = p + lane;
+      if (pl < p1) {
+        const int r = rowid(pl);
+        c_row = r;
+        c_vco = __ldcg(v.vco + r);
+        c_dco = __ldcg(v.dco + r);
+        c_J = __ldcg(v.gJ + r);
+        c_vsg = __ldcg(v.vsg + r);
+        c_k1 = __ldg(P.k1 + o + r);
+        c_k2 = __ldg(P.k2 + o + r);
+      }
+    }
+    // assemble up to four entries whose rows fit in the ring window
+    int nent = 0, q0 = 0, my_q = 0, my_i = 0, last_q = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (p + g < p1) {
+        const int i = __shfl_sync(FULL, c_row, p + g - cbase);
+        int q_im1, hi = st.hi_c, qhi = st.qhi_c;
+        if (i - 1 > hi) {
+          q_im1 = qhi + 1;
+          qhi += 3;
+        } else {
+          qhi += (i + 1) - hi;
+          q_im1 = qhi - 2;
+        }
+        if (g == 0) q0 = q_im1;
+        if (g == 0 || q_im1 + 2 - q0 + 1 <= S) {
+          if (nent == g) {
+            st.hi_c = i + 1;
+            st.qhi_c = qhi;
+            nent = g + 1;
+            last_q = q_im1;
+            if (g == gr) {
+              my_q = q_im1;
+              my_i = i;
+            }
+          }
+        }
+      }
+    }
+    const bool active = gr < nent;
+    double out_lo[CH], out_hi[CH];
+    const int i = my_i;
+    // coefficient broadcast (all lanes take part in the shuffles)
+    const int src = min(p + gr - cbase, 31);
+    const int vsg = __shfl_sync(FULL, c_vsg, src);
+    const double vco = __shfl_sync(FULL, c_vco, src);
+    const double dc = __shfl_sync(FULL, c_dco, src);
+    const double J = __shfl_sync(FULL, c_J, src);
+    const double k1 = __shfl_sync(FULL, c_k1, src);
+    const double k2 = __shfl_sync(FULL, c_k2, src);
+    if (active) {
+      const uint32_t rp = slot_addr(my_q), rcu = slot_addr(my_q + 1), rn = slot_addr(my_q + 2);
+#pragma unroll
+      for (int mm = 0; mm < CH; ++mm) {
+        // lower half: column c = k + 8mm, xi < 0: x-upwind uses row i+1
+        {
+          const int c = k + 8 * mm;
+          const double g = lds64(rcu + 8 * c);
+          const double xi = lds64(s_vx + 8 * c);
+          double oo = xi * (lds64(rn + 8 * c) - g);
+          oo = qdiv(oo, dx, rdx);
+          // velocity upwind by sign(E), zero inflow at -v* (kinetic.py:176-187)
+          const int cn = vsg > 0 ? c - 1 : c + 1;
+          const double nb = cn >= 0 ? lds64(rcu + 8 * cn) : 0.0;
+          const double d = vsg > 0 ? g - nb : nb - g;
+          if (vsg != 0) oo = oo + d * vco;
+          oo = oo - lds64(s_M + 8 * c) * dc;
+          const double forcing = oo + lds64(s_xiM + 8 * c) * J;
+          out_lo[mm] = k1 * g - k2 * forcing;
+        }
+        // upper half: column u = nv-1-c, xi > 0: x-upwind uses row i-1
+        {
+          const int u = NV - 1 - k - 8 * mm;
+          const double g = lds64(rcu + 8 * u);
+          const double xi = lds64(s_vx + 8 * u);
+          double oo = xi * (g - lds64(rp + 8 * u));
+          oo = qdiv(oo, dx, rdx);
+          // zero inflow at +v*
+          const int un = vsg > 0 ? u - 1 : u + 1;
+          const double nb = un < NV ? lds64(rcu + 8 * un) : 0.0;
+          const double d = vsg > 0 ? g - nb : nb - g;
+          if (vsg != 0) oo = oo + d * vco;
+          oo = oo - lds64(s_M + 8 * u) * dc;
+          const double forcing = oo + lds64(s_xiM + 8 * u) * J;
+          out_hi[mm] = k1 * g - k2 * forcing;
+        }
+      }
+    }
+    __syncwarp();
+    pump(last_q + 1 + S);  // positions < pos(last row) are consumed
+    if (active) {
+      double* row = gout + (size_t)i * NV;
+#pragma unroll
+      for (int mm = 0; mm < CH; ++mm) {
+        __stcg(row + k + 8 * mm, out_lo[mm]);
+        __stcg(row + NV - 1 - k - 8 * mm, out_hi[mm]);
+      }
+    }
+    // row moments: fold, in-lane pairwise chain k, 8-way tree (mesh.py:95-133)
+    double bx = 0.0, bsq = 0.0;
+    if (active) {
+#pragma unroll
+      for (int mm = 0; mm < CH; ++mm) {
+        const int c = k + 8 * mm, u = NV - 1 - c;
+        const double f = lds64(s_vx + 8 * c) * out_lo[mm] + lds64(s_vx + 8 * u) * out_hi[mm];
+        const double h = out_lo[mm] * out_lo[mm] + out_hi[mm] * out_hi[mm];
+        bx = mm == 0 ? f : bx + f;
+        bsq = mm == 0 ? h : bsq + h;
+      }
+    }
+    bx = bx + __shfl_xor_sync(FULL, bx, 1);
+    bx = bx + __shfl_xor_sync(FULL, bx, 2);
+    bx = bx + __shfl_xor_sync(FULL, bx, 4);
+    bsq = bsq + __shfl_xor_sync(FULL, bsq, 1);
+    bsq = bsq + __shfl_xor_sync(FULL, bsq, 2);
+    bsq = bsq + __shfl_xor_sync(FULL, bsq, 4);
+    if (active && k == 0) {
+      v.fl_w[i] = bx * dv3;
+      v.sq_w[i] = bsq * dv3;
+    }
+    p += nent;
+  }
+  qbase += (uint32_t)st.q_prod;
+}
+
 // Micro phase, generic layout (any nv <= 256, no TMA): direct row loads.
 __device__ void micro_phase_gen(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                 const double* gin, double* gout, int wg, int nwg) {
@@ -794,8 +999,9 @@ __device__ __forceinline__ void cluster_barrier(int C) {
   }
 }
 
-template <int T, int S>
-__global__ void __launch_bounds__(256, 2) fine_kernel(const FineArgs a) {
+template <int T, int S, int G, int NT>
+__global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
+  constexpr int RSN = G != 0 ? 16 * G + 8 : 32 * T;  // ring row stride (doubles)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
@@ -831,7 +1037,7 @@ __global__ void __launch_bounds__(256, 2) fine_kernel(const FineArgs a) {
     if (T == 0) p += (size_t)nwpc * nv * 8;  // generic-layout row scratch
     if (T != 0) {
       ring = reinterpret_cast<double*>(p);
-      p += (size_t)nwpc * S * nv * 8;
+      p += (size_t)nwpc * S * RSN * 8;
     }
     if (a.local_smem) sm_loc = reinterpret_cast<double*>(p);  // same offset in every CTA
   }
@@ -866,7 +1072,7 @@ __global__ void __launch_bounds__(256, 2) fine_kernel(const FineArgs a) {
   int* abort_flag = v.abort_;
   const size_t o = (size_t)b * nx;
   uint32_t qbase = 0;
-  double* ring_w = ring ? ring + (size_t)warp * S * nv : nullptr;
+  double* ring_w = ring ? ring + (size_t)warp * S * RSN : nullptr;
   uint64_t* mbar_w = mbar + warp * S;
 
   // ---- prologue ----
@@ -928,7 +1134,9 @@ __global__ void __launch_bounds__(256, 2) fine_kernel(const FineArgs a) {
   long long c0 = prof ? clock64() : 0, c1;
   for (int s = 0; s < nst; ++s) {
     const int ph = s < n0 ? 0 : 1;
-    if constexpr (T != 0)
+    if constexpr (G != 0)
+      micro_phase_g8<G, S>(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg, ring_w, mbar_w, qbase);
+    else if constexpr (T != 0)
       micro_phase_tma<T, S>(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg, ring_w, mbar_w, qbase);
     else
       micro_phase_gen(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
@@ -1080,11 +1288,11 @@ __global__ void __launch_bounds__(256) field_kernel(const FieldArgs a) {
 
 constexpr int kThreads = 256;
 
-static size_t base_smem(int nv, int T, int S) {
+static size_t base_smem(int nv, int T, int S, int G, int NT) {
   size_t s = 64 * 8 + (sizeof(PwPlan) + 15) / 16 * 16 + 4 * (size_t)nv * 8 +
              2 * (MAX_LEAF + MAX_NODE) * 8 + 64 * 4;
-  if (T == 0) s += (kThreads / 32) * (size_t)nv * 8;
-  else s += (size_t)(kThreads / 32) * S * nv * 8;
+  if (T == 0) s += (NT / 32) * (size_t)nv * 8;
+  else s += (size_t)(NT / 32) * S * (G != 0 ? nv + 8 : nv) * 8;
   return s;
 }
 
@@ -1093,9 +1301,9 @@ static size_t local_smem(int nx, int adaptation) {
                     : (size_t)nx * (NLOC_DK * 8 + NLOC_BK) + 16;
 }
 
-template <int T, int S>
+template <int T, int S, int G, int NT>
 static cudaError_t launch_T(FineArgs a, int C, cudaStream_t st) {
-  const size_t base = base_smem(a.m.nv, T, S);
+  const size_t base = base_smem(a.m.nv, T, S, G, NT);
   // slice vectors on chip when two CTAs still fit per SM
   size_t smem = base;
   a.local_smem = 0;
@@ -1103,7 +1311,7 @@ static cudaError_t launch_T(FineArgs a, int C, cudaStream_t st) {
     a.local_smem = 1;
     smem = base + local_smem(a.m.nx, a.adaptation);
   }
-  auto kern = fine_kernel<T, S>;
+  auto kern = fine_kernel<T, S, G, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (C > 8) {
@@ -1112,7 +1320,7 @@ static cudaError_t launch_T(FineArgs a, int C, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.B * C);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1158,12 +1366,12 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
 
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   switch (a.m.nv) {
-    case 64: return launch_T<2, 6>(a, C, st);
-    case 128: return launch_T<4, 4>(a, C, st);
-    case 256: return launch_T<8, 3>(a, C, st);
-    case 512: return launch_T<16, 3>(a, C, st);
+    case 64: return launch_T<2, 12, 4, 128>(a, C, st);   // G8 layout, 4 warps
+    case 128: return launch_T<4, 11, 8, 128>(a, C, st);  // G8 layout, 4 warps
+    case 256: return launch_T<8, 3, 0, 256>(a, C, st);
+    case 512: return launch_T<16, 3, 0, 256>(a, C, st);
     default:
-      if (a.m.nv <= 32 * GT) return launch_T<0, 1>(a, C, st);
+      if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
       return cudaErrorInvalidValue;
   }
 }
