@@ -280,7 +280,7 @@ def main():
         with open(tpath) as f:
             tr = json.load(f)
         if tr.get("nv") == NV and tr.get("nx") == NX:
-            traffic = tr.get("bytes_per_update")
+            traffic = tr.get("bytes_per_launch")
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline()

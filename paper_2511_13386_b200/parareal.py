@@ -45,6 +45,7 @@ from .mesh import MacroState, MicroState, PhaseMesh
 from .poisson import SOLVABILITY_RTOL, solve_field
 
 WORKERS_ENV = "PARAKIN_WORKERS"
+_BACKEND = None   # engine backend factory; None = DeviceBackend (tests inject a CPU one)
 ADAPTIVE_FIELD_RTOL = 1e-5
 
 
@@ -156,23 +157,127 @@ class _Comm:
 
 
 # ---------------------------------------------------------------------------
-# device engine
+# engine: coordination logic over a backend of five primitives
+
+
+class DeviceBackend:
+    """The product backend: libpk kernels on this rank's CUDA device.
+
+    ``fine``   all listed windows in ONE persistent-kernel launch
+               (pk_fine_propagate; window 1 from g0, others lifted);
+    ``chain``  one CTA walks consecutive windows sequentially
+               (pk_coarse_chain), optionally adding the jumps;
+    ``many``   independent single-window G chains (cold G cache);
+    ``jump`` / ``maxdiff``  Delta = F - G and max|a - b| with the
+               reference's non-finite checks (parareal.py:267-269,283-286).
+    """
+
+    def __init__(self, eng):
+        import torch
+
+        self.torch = torch
+        self.eng = eng
+        self.dev = Device.for_mesh(eng.mesh)
+        self.device = self.dev.device
+        self.rb1 = self.dev.t(np.array([eng.rho_bar]))
+        self.g0 = self.dev.t(np.ascontiguousarray(np.asarray(eng.g0, float).reshape(eng.nx, eng.nv)))
+        self.err_d = torch.zeros(1, dtype=torch.float64, device=self.device)
+
+    def tensor(self, a):
+        return self.dev.t(np.ascontiguousarray(a, dtype=float))
+
+    def chain(self, x, n0, n1, delta, rtol):
+        e = self.eng
+        W = n1 - n0 + 1
+        out = self.torch.empty((W, e.nx), dtype=self.torch.float64, device=self.device)
+        gout = self.torch.empty_like(out)
+        sc = e.sc[n0 - 1:n1]
+        self.dev.chain(x.reshape(1, e.nx), out.reshape(1, W, e.nx), gout.reshape(1, W, e.nx), None,
+                       None if delta is None else delta.reshape(1, W, e.nx),
+                       [q[0] for q in sc], [q[1] for q in sc], e.fluid_p.dt, self.rb1,
+                       SOLVABILITY_RTOL if rtol is None else rtol, m2=e.fluid_p.m2)
+        self.dev.check()
+        return out, gout
+
+    def many(self, X, windows, rtol):
+        e = self.eng
+        B = len(windows)
+        out = self.torch.empty((B, 1, e.nx), dtype=self.torch.float64, device=self.device)
+        sc = [e.sc[n - 1] for n in windows]
+        self.dev.chain(X.contiguous(), out, None, None, None, [q[0] for q in sc],
+                       [q[1] for q in sc], e.fluid_p.dt, self.rb1.expand(B).contiguous(),
+                       SOLVABILITY_RTOL if rtol is None else rtol, m2=e.fluid_p.m2)
+        self.dev.check()
+        return out[:, 0]
+
+    def fine(self, X, windows):
+        torch, dev, e = self.torch, self.dev, self.eng
+        B = len(windows)
+        nx, nv = e.nx, e.nv
+        rho = X.clone()
+        g = dev.scratch("par_g", (B, nx, nv))
+        flags = []
+        for i, n in enumerate(windows):
+            if n == 1:
+                g[i].copy_(self.g0)
+                flags.append(2)      # true g0, E_prev := E  (parareal.py:169-170,178)
+            else:
+                flags.append(3)      # lifted g, E_prev := E
+        E = torch.empty((B, nx), dtype=torch.float64, device=self.device)
+        Ep = torch.empty_like(E)
+        kc = torch.ones((B, nx), dtype=torch.uint8, device=self.device)
+        ki = torch.ones_like(kc)
+        eps = [e.cfg.eps] * B
+        dt = e.kin_p.dt
+        ph0 = make_phase(e.mesh, eps, [dt] * B, [e.sf[n - 1][0] for n in windows])
+        ph1 = make_phase(e.mesh, eps,
+                         [e.sf[n - 1][1] if e.sf[n - 1][1] > 0.0 else dt for n in windows],
+                         [1 if e.sf[n - 1][1] > 0.0 else 0 for n in windows])
+        dev.fine(rho, E, Ep, kc, ki, g, self.rb1.expand(B).contiguous(), flags, [ph0, ph1],
+                 e.knobs, eps, e.rtol_f)
+        dev.check()
+        return rho, kc.sum(dim=1, dtype=torch.int64)
+
+    def jump(self, F, G):
+        delta = self.torch.empty_like(F)
+        self.dev.jump(F, G, delta)
+        self.dev.check()
+        return delta
+
+    def maxdiff(self, a, b):
+        self.dev.maxdiff(a, b, self.err_d)
+        err = float(self.err_d.item())
+        self.dev.check()
+        return err
+
+    def clock(self):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    @staticmethod
+    def seconds(a, b):
+        return a.elapsed_time(b) * 1e-3
 
 
 class _Engine:
-    """Device-resident state of one parareal run."""
+    """State and coordination of one parareal run (parareal.py:210-310).
 
-    def __init__(self, cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p, comm=None):
+    Rows live on the backend's device; ``G[n]`` caches G(row_k[n-1]).  With
+    a communicator of size > 1 the active windows are dealt cyclically to
+    ranks, fine results are all-gathered, and every rank runs the
+    (deterministic) correction itself, so ledgers agree bit for bit."""
+
+    def __init__(self, cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p, comm=None, backend=None):
         import torch
 
         self.torch = torch
         self.cfg, self.mesh, self.fluid_p, self.kin_p = cfg, mesh, fluid_p, kin_p
-        self.dev = Device.for_mesh(mesh)
         self.comm = comm or _Comm()
         self.rho_bar = float(rho_bar)
-        self.nx, self.nv, ng = mesh.nx, mesh.nv, cfg.ng
+        self.g0 = g0
+        self.nx, self.nv, ng = mesh.nx, mesh.vgrid.vx.shape[0], cfg.ng
         b = cfg.boundaries
-        self.bounds = b
         self.sc = [substep_sizes(float(b[n - 1]), float(b[n]), fluid_p.dt) for n in range(1, ng + 1)]
         self.sf = [substep_sizes(float(b[n - 1]), float(b[n]), kin_p.dt) for n in range(1, ng + 1)]
         for nf, rem in self.sc:
@@ -187,120 +292,72 @@ class _Engine:
                 kin_p.check(rem, mesh)
         self.rtol = field_guard(cfg)
         self.rtol_f = SOLVABILITY_RTOL if self.rtol is None else self.rtol
-        dev = self.dev
-        self.row = dev.t(np.ascontiguousarray(np.repeat(np.asarray(rho0, float)[None], ng + 1, 0)))
-        self.G = torch.empty_like(self.row)    # G[n] = G(row_k[n-1])
-        self.g0 = dev.t(np.ascontiguousarray(np.asarray(g0, float).reshape(self.nx, self.nv)))
-        self.rb1 = dev.t(np.array([self.rho_bar]))
         self.knobs = knobs_of(cfg.options, cfg.thresholds)
-        self.err_d = torch.zeros(1, dtype=torch.float64, device=dev.device)
-
-    # coarse chain over windows n0..n1 (1-based, inclusive) starting from x
-    def _chain(self, x, n0, n1, out, gout, delta, rtol):
-        sc = self.sc[n0 - 1:n1]
-        self.dev.chain(x.reshape(1, self.nx), out.reshape(1, -1, self.nx),
-                       None if gout is None else gout.reshape(1, -1, self.nx), None,
-                       None if delta is None else delta.reshape(1, -1, self.nx),
-                       [s[0] for s in sc], [s[1] for s in sc], self.fluid_p.dt, self.rb1,
-                       SOLVABILITY_RTOL if rtol is None else rtol, m2=self.fluid_p.m2)
+        self.be = backend(self) if backend is not None else DeviceBackend(self)
+        self.row = self.be.tensor(np.repeat(np.asarray(rho0, float)[None], ng + 1, 0))
+        self.G = torch.empty_like(self.row)
 
     def coarse_sweep(self):
-        ng = self.cfg.ng
-        self._chain(self.row[0], 1, ng, self.row[1:], None, None, None)
-        self.G[1:] = self.row[1:]   # G(row_0[n-1]) == row_0[n]
-        self.dev.check()
+        """Row 0 (parareal.py:210-229); default field guard as the reference."""
+        out, _ = self.be.chain(self.row[0], 1, self.cfg.ng, None, None)
+        self.row[1:] = out
+        self.G[1:] = out   # G(row_0[n-1]) == row_0[n] (SURVEY F12)
 
-    def fine(self, windows):
-        """F for the given windows (this rank's share); returns (rho_out, kc)."""
-        torch, dev = self.torch, self.dev
-        B = len(windows)
-        nx, nv = self.nx, self.nv
-        rho = self.row[[n - 1 for n in windows]].clone()
-        g = dev.scratch("par_g", (B, nx, nv))
-        flags = []
-        for i, n in enumerate(windows):
-            if n == 1:
-                g[i].copy_(self.g0)
-                flags.append(2)      # true g0, E_prev := E  (parareal.py:169-170,178)
-            else:
-                flags.append(3)      # lifted g, E_prev := E
-        E = torch.empty((B, nx), dtype=torch.float64, device=dev.device)
-        Ep = torch.empty_like(E)
-        kc = torch.ones((B, nx), dtype=torch.uint8, device=dev.device)
-        ki = torch.ones_like(kc)
-        eps = [self.cfg.eps] * B
-        dt = self.kin_p.dt
-        ph0 = make_phase(self.mesh, eps, [dt] * B, [self.sf[n - 1][0] for n in windows])
-        ph1 = make_phase(self.mesh, eps,
-                         [self.sf[n - 1][1] if self.sf[n - 1][1] > 0.0 else dt for n in windows],
-                         [1 if self.sf[n - 1][1] > 0.0 else 0 for n in windows])
-        dev.fine(rho, E, Ep, kc, ki, g, self.rb1.expand(B).contiguous(), flags, [ph0, ph1],
-                 self.knobs, eps, self.rtol_f)
-        return rho, kc
+    def cold_G(self, k):
+        """G(row_k[n-1]) for n = k+1..Ng (independent chains)."""
+        wins = list(range(k + 1, self.cfg.ng + 1))
+        if wins:
+            self.G[k + 1:] = self.be.many(self.row[k:self.cfg.ng], wins, self.rtol)
 
     def iterate(self, k):
-        torch, dev, cfg = self.torch, self.dev, self.cfg
+        torch, cfg, be = self.torch, self.cfg, self.be
         ng, nx = cfg.ng, self.nx
         targets = list(range(k + 1, ng + 1))
         B = len(targets)
         if B == 0:
             # every window converged by prefix exactness: row_{k+1} == row_k
-            return 0.0, torch.empty((0, nx), dtype=torch.float64, device=dev.device), \
-                np.zeros(ng + 1), targets, 0.0, 0.0
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        ev[0].record()
-        # this rank's windows: cyclic deal
-        mine = targets[self.comm.rank::self.comm.size]
-        Fall = torch.empty((B, nx), dtype=torch.float64, device=dev.device)
-        fracs = np.zeros(ng + 1)
-        if self.comm.size == 1:
-            Fr, kc = self.fine(targets)
-            Fall.copy_(Fr)
-            kcount = kc.sum(dim=1, dtype=torch.int64)
+            return 0.0, self.row[:0], np.zeros(ng + 1), targets, 0.0, 0.0
+        t0 = be.clock()
+        size, rank = self.comm.size, self.comm.rank
+        if size == 1:
+            Fall, kcount = be.fine(self.row[k:ng], targets)
         else:
-            per = -(-B // self.comm.size)
+            # cyclic deal; one all-gather of [per + 1, nx] rows per rank (the
+            # extra row carries the kinetic-cell counts)
+            per = -(-B // size)
             assert per <= nx, "window share exceeds the gather row width"
-            buf = torch.zeros((per + 1, nx), dtype=torch.float64, device=dev.device)
+            mine = targets[rank::size]
+            buf = torch.zeros((per + 1, nx), dtype=torch.float64, device=self.row.device)
             if mine:
-                Fr, kc = self.fine(mine)
+                Fr, kc = be.fine(self.row[[n - 1 for n in mine]], mine)
                 buf[:len(mine)] = Fr
-                buf[per, :len(mine)] = kc.sum(dim=1, dtype=torch.int64).to(torch.float64)
+                buf[per, :len(mine)] = kc.to(torch.float64)
             parts = self.comm.all_gather(buf)
-            kcount = torch.empty(B, dtype=torch.int64, device=dev.device)
+            Fall = torch.empty((B, nx), dtype=torch.float64, device=self.row.device)
+            kcount = torch.empty(B, dtype=torch.int64, device=self.row.device)
             for r, part in enumerate(parts):
-                wins = targets[r::self.comm.size]
-                for j, n in enumerate(wins):
+                for j, n in enumerate(targets[r::size]):
                     Fall[n - k - 1] = part[j]
                     kcount[n - k - 1] = part[per, j].to(torch.int64)
-        ev[1].record()
-        delta = torch.empty_like(Fall)
-        dev.jump(Fall, self.G[k + 1:], delta)
-        dev.check()   # NonFiniteState from the jumps (parareal.py:267-269)
-        ev[2].record()
+        t1 = be.clock()
+        delta = be.jump(Fall, self.G[k + 1:])   # NonFiniteState (parareal.py:267-269)
+        t2 = be.clock()
         new = self.row.clone()
         Gn = self.G.clone()
-        self._chain(self.row[k], k + 1, ng, new[k + 1:], Gn[k + 1:], delta, self.rtol)
-        ev[3].record()
-        dev.maxdiff(new, self.row, self.err_d)
-        err = float(self.err_d.item())
-        dev.check()   # NonFiniteState after the correction (parareal.py:283-284)
+        out, gout = be.chain(self.row[k], k + 1, ng, delta, self.rtol)
+        new[k + 1:] = out
+        Gn[k + 1:] = gout
+        t3 = be.clock()
+        err = be.maxdiff(new, self.row)          # NonFiniteState (parareal.py:283-284)
+        fracs = np.zeros(ng + 1)
+        kc_h = kcount.cpu().numpy()
         for j, n in enumerate(targets):
-            fracs[n] = float(kcount[j].item()) / nx
-        t_fine = ev[0].elapsed_time(ev[1]) * 1e-3
-        t_corr = ev[2].elapsed_time(ev[3]) * 1e-3
+            fracs[n] = float(kc_h[j]) / nx
         self.row, self.G = new, Gn
-        return err, delta, fracs, targets, t_fine, t_corr
+        return err, delta, fracs, targets, be.seconds(t0, t1), be.seconds(t2, t3)
 
 
 _ENGINES: dict = {}
-
-
-def _engine_for(ledger, cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p):
-    eng = _ENGINES.get(id(ledger))
-    if eng is None or eng.cfg is not cfg:
-        eng = _Engine(cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p)
-        _ENGINES[id(ledger)] = eng
-    return eng
 
 
 # ---------------------------------------------------------------------------
@@ -352,7 +409,7 @@ def coarse_sweep(rho0, cfg: PararealConfig, fluid_p: FluidStepParams, mesh: Phas
         kin_p = KineticStepParams(eps=cfg.eps, dt=fluid_p.dt)
     if g0 is None:
         g0 = np.zeros((mesh.nx,) + mesh.vgrid.shape)
-    eng = _Engine(cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p)
+    eng = _Engine(cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p, backend=_BACKEND)
     eng.coarse_sweep()
     _ENGINES[id(ledger)] = eng
     ledger.rho.append(eng.row.cpu().numpy())
@@ -372,9 +429,10 @@ def parareal_iterate(ledger: PararealLedger, k: int, cfg: PararealConfig,
         return _iterate_host_seam(ledger, k, cfg, fluid_p, kin_p, mesh, rho_bar, g0, iter_tic)
     eng = _ENGINES.get(id(ledger))
     if eng is None or eng.kin_p is not kin_p or k != len(ledger.rho) - 1:
-        eng = _Engine(cfg, mesh, ledger.rho[0][0], g0, rho_bar, fluid_p, kin_p)
-        eng.row = eng.dev.t(np.ascontiguousarray(ledger.rho[k]))
-        _recompute_G(eng, k)   # G(row_k[n-1]) for the active windows
+        eng = _Engine(cfg, mesh, ledger.rho[0][0], g0, rho_bar, fluid_p, kin_p,
+                      backend=_BACKEND)
+        eng.row = eng.be.tensor(ledger.rho[k])
+        eng.cold_G(k)   # G(row_k[n-1]) for the active windows
         _ENGINES[id(ledger)] = eng
     err, delta, fracs, targets, t_fine, t_corr = eng.iterate(k)
     ledger.rho.append(eng.row.cpu().numpy())
@@ -390,22 +448,6 @@ def parareal_iterate(ledger: PararealLedger, k: int, cfg: PararealConfig,
     tm.iterations.append({"k": k + 1, "err": err, "parallel_s": t_fine, "correction_s": t_corr,
                           "wall_s": time.perf_counter() - iter_tic})
     return err
-
-
-def _recompute_G(eng: _Engine, k: int):
-    """G(row_k[n-1]) for n = k+1..Ng as independent chains (cold start)."""
-    torch = eng.torch
-    ng = eng.cfg.ng
-    B = ng - k
-    if B <= 0:
-        return
-    out = torch.empty((B, 1, eng.nx), dtype=torch.float64, device=eng.dev.device)
-    sc = eng.sc[k:ng]
-    eng.dev.chain(eng.row[k:ng].contiguous(), out, None, None, None,
-                  [s[0] for s in sc], [s[1] for s in sc], eng.fluid_p.dt,
-                  eng.rb1.expand(B).contiguous(), eng.rtol_f, m2=eng.fluid_p.m2)
-    eng.G[k + 1:] = out[:, 0]
-    eng.dev.check()
 
 
 def _iterate_host_seam(ledger, k, cfg, fluid_p, kin_p, mesh, rho_bar, g0, iter_tic):
