@@ -10,8 +10,8 @@
 namespace pk {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int MAX_LEAF = 160;   // pairwise leaves of <= 128 terms: nx <= 20480
-constexpr int MAX_NODE = 160;
+constexpr int MAX_LEAF = 80;    // pairwise leaves of <= 128 terms: nx <= 10240
+constexpr int MAX_NODE = 80;
 constexpr int MAX_LEVEL = 10;
 
 // Correctly rounded x / d from rd = RN(1/d): one Markstein correction step.

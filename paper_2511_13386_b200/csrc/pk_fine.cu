@@ -675,31 +675,28 @@ __device__ void micro_phase_tma(const FineArgs& a, const SliceView& v, const Sme
 // Every operand (row i, its x-neighbours, the velocity neighbours) is read
 // from the TMA ring in shared memory; ring rows are padded by 64 B so the
 // four groups of a warp hit distinct bank halves.
-template <int CH, int S>
+template <int CH, int S, bool DENSE>
 __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
-                               const double* gin, double* gout, int wg, int nwg, double* ring,
+                               const double* gin, double* gout, int p0, int p1, double* ring,
                                uint64_t* mbar, uint32_t& qbase) {
   constexpr int NV = 16 * CH;
-  constexpr int RS = NV + 8;  // ring row stride in doubles
+  constexpr int RS = NV + 8;  // ring row stride in doubles (64 B pad)
   const MeshDev& m = a.m;
   const int nx = m.nx;
   const int lane = threadIdx.x & 31;
   const int k = lane & 7, gr = lane >> 3;
-  const int nk = __ldcg(v.nk);
-  const bool dense = nk == nx;
-  const int p0 = (int)(((long long)wg * nk) / nwg);
-  const int p1 = (int)(((long long)(wg + 1) * nk) / nwg);
-  if (p0 >= p1) return;
   const PhaseDev& P = a.ph[ph];
   const size_t o = (size_t)v.b * nx;
   const uint32_t s_vx = smem_u32(sm.vx), s_M = smem_u32(sm.M), s_xiM = smem_u32(sm.xiM);
-  const uint32_t s_ring = smem_u32(ring);
+  const uint32_t s_ring = smem_u32(ring), s_mbar = smem_u32(mbar);
   const double dx = m.dx, rdx = m.rdx, dv3 = m.dv3;
-  auto rowid = [&](int p) { return dense ? p : __ldcg(v.klist + p); };
+  auto rowid = [&](int p) { return DENSE ? p : __ldcg(v.klist + p); };
 
   if (lane == 0) fence_proxy_async_global();  // rows written by the generic proxy, read by TMA
   __syncwarp();
 
+  // ---- row stream: producer (lane 0 issues) and consumer position logic ----
+  // DENSE: the stream is rows p0-1 .. p1, position q <-> row p0-1+q.
   RowStream st;
   st.p_prod = p0;
   st.e_next = 1;
@@ -708,8 +705,28 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   st.q_prod = 0;
   st.hi_c = -3;
   st.qhi_c = -1;
+  const int q_end = DENSE ? (p1 - p0 + 2) : 0x7fffffff;
   constexpr uint32_t bytes = NV * 8;
+  auto issue = [&](int q, int row) {
+    if (lane == 0) {
+      const uint32_t Q = qbase + (uint32_t)q;
+      const uint32_t slot = Q % S;
+      const uint32_t mb = s_mbar + 8 * slot;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(s_ring + slot * (RS * 8)),
+          "l"(gin + (size_t)wrap(row, nx) * NV), "r"(bytes), "r"(mb)
+          : "memory");
+    }
+  };
   auto pump = [&](int q_limit) {
+    if (DENSE) {
+      const int lim = min(q_limit, q_end);
+      for (; st.q_prod < lim; ++st.q_prod) issue(st.q_prod, p0 - 1 + st.q_prod);
+      return;
+    }
     while (st.q_prod < q_limit) {
       if (st.e_next > st.e_end) {
         if (st.p_prod >= p1) break;
@@ -718,12 +735,7 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
         st.e_end = i + 1;
         continue;
       }
-      if (lane == 0) {
-        const uint32_t Q = qbase + (uint32_t)st.q_prod;
-        const int slot = (int)(Q % S);
-        mbar_expect_tx(mbar + slot, bytes);
-        bulk_g2s(ring + slot * RS, gin + (size_t)wrap(st.e_next, nx) * NV, bytes, mbar + slot);
-      }
+      issue(st.q_prod, st.e_next);
       st.hi_p = st.e_next;
       ++st.e_next;
       ++st.q_prod;
@@ -731,14 +743,22 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   };
   auto slot_addr = [&](int q) {
     const uint32_t Q = qbase + (uint32_t)q;
-    const int slot = (int)(Q % S);
-    mbar_wait(mbar + slot, (Q / S) & 1);
-    return s_ring + (uint32_t)(slot * RS * 8);
+    const uint32_t slot = Q % S;
+    const uint32_t mb = s_mbar + 8 * slot, par = (Q / S) & 1;
+    uint32_t done;
+    do {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(mb), "r"(par)
+          : "memory");
+    } while (!done);
+    return s_ring + slot * (RS * 8);
   };
 
   pump(S);
   double c_vco = 0, c_dco = 0, c_J = 0, c_k1 = 0, c_k2 = 0;
-  int c_vsg = 0, c_row = 0;
+  int c_row = 0;
   int cbase = p0 - 64;
   for (int p = p0; p < p1;) {
     if (p + 4 - cbase > 32) {
@@ -747,114 +767,105 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
       if (pl < p1) {
         const int r = rowid(pl);
         c_row = r;
-        c_vco = __ldcg(v.vco + r);
+        // signed E-upwind factor: (g - g_nb) * (+-vco) reproduces both of the
+        // reference's forms bitwise (kinetic.py:176-187); 0 when E == 0
+        const int sg = __ldcg(v.vsg + r);
+        const double vco = __ldcg(v.vco + r);
+        c_vco = sg > 0 ? vco : (sg < 0 ? -vco : 0.0);
         c_dco = __ldcg(v.dco + r);
         c_J = __ldcg(v.gJ + r);
-        c_vsg = __ldcg(v.vsg + r);
         c_k1 = __ldg(P.k1 + o + r);
         c_k2 = __ldg(P.k2 + o + r);
+        // neighbour direction rides in the sign bit of the row id
+        c_row = sg > 0 ? r : -1 - r;
       }
     }
-    // assemble up to four entries whose rows fit in the ring window
-    int nent = 0, q0 = 0, my_q = 0, my_i = 0, last_q = 0;
+    // entries of this operation (up to four, within the ring window)
+    int nent, my_q, last_q;
+    if (DENSE) {
+      nent = min(4, p1 - p);
+      my_q = p + gr - p0;            // position of row (p+gr)-1
+      last_q = p + nent - 1 - p0;
+    } else {
+      nent = 0;
+      my_q = 0;
+      last_q = 0;
+      int q0 = 0;
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      if (p + g < p1) {
-        const int i = __shfl_sync(FULL, c_row, p + g - cbase);
-        int q_im1, hi = st.hi_c, qhi = st.qhi_c;
-        if (i - 1 > hi) {
-          q_im1 = qhi + 1;
-          qhi += 3;
-        } else {
-          qhi += (i + 1) - hi;
-          q_im1 = qhi - 2;
-        }
-        if (g == 0) q0 = q_im1;
-        if (g == 0 || q_im1 + 2 - q0 + 1 <= S) {
-          if (nent == g) {
+      for (int g = 0; g < 4; ++g) {
+        if (p + g < p1 && nent == g) {
+          int i = __shfl_sync(FULL, c_row, p + g - cbase);
+          i = i < 0 ? -1 - i : i;
+          int q_im1, hi = st.hi_c, qhi = st.qhi_c;
+          if (i - 1 > hi) {
+            q_im1 = qhi + 1;
+            qhi += 3;
+          } else {
+            qhi += (i + 1) - hi;
+            q_im1 = qhi - 2;
+          }
+          if (g == 0) q0 = q_im1;
+          if (g == 0 || q_im1 + 2 - q0 + 1 <= S) {
             st.hi_c = i + 1;
             st.qhi_c = qhi;
             nent = g + 1;
             last_q = q_im1;
-            if (g == gr) {
-              my_q = q_im1;
-              my_i = i;
-            }
+            if (g == gr) my_q = q_im1;
           }
         }
       }
     }
     const bool active = gr < nent;
-    double out_lo[CH], out_hi[CH];
-    const int i = my_i;
-    // coefficient broadcast (all lanes take part in the shuffles)
     const int src = min(p + gr - cbase, 31);
-    const int vsg = __shfl_sync(FULL, c_vsg, src);
-    const double vco = __shfl_sync(FULL, c_vco, src);
+    const int rsg = __shfl_sync(FULL, c_row, src);
+    const double svco = __shfl_sync(FULL, c_vco, src);
     const double dc = __shfl_sync(FULL, c_dco, src);
     const double J = __shfl_sync(FULL, c_J, src);
     const double k1 = __shfl_sync(FULL, c_k1, src);
     const double k2 = __shfl_sync(FULL, c_k2, src);
+    const bool up = rsg >= 0;          // E > 0 (or 0): velocity neighbour j-1
+    const int i = up ? rsg : -1 - rsg;
+    double bx = 0.0, bsq = 0.0;
     if (active) {
       const uint32_t rp = slot_addr(my_q), rcu = slot_addr(my_q + 1), rn = slot_addr(my_q + 2);
-#pragma unroll
-      for (int mm = 0; mm < CH; ++mm) {
-        // lower half: column c = k + 8mm, xi < 0: x-upwind uses row i+1
-        {
-          const int c = k + 8 * mm;
-          const double g = lds64(rcu + 8 * c);
-          const double xi = lds64(s_vx + 8 * c);
-          double oo = xi * (lds64(rn + 8 * c) - g);
-          oo = qdiv(oo, dx, rdx);
-          // velocity upwind by sign(E), zero inflow at -v* (kinetic.py:176-187)
-          const int cn = vsg > 0 ? c - 1 : c + 1;
-          const double nb = cn >= 0 ? lds64(rcu + 8 * cn) : 0.0;
-          const double d = vsg > 0 ? g - nb : nb - g;
-          if (vsg != 0) oo = oo + d * vco;
-          oo = oo - lds64(s_M + 8 * c) * dc;
-          const double forcing = oo + lds64(s_xiM + 8 * c) * J;
-          out_lo[mm] = k1 * g - k2 * forcing;
-        }
-        // upper half: column u = nv-1-c, xi > 0: x-upwind uses row i-1
-        {
-          const int u = NV - 1 - k - 8 * mm;
-          const double g = lds64(rcu + 8 * u);
-          const double xi = lds64(s_vx + 8 * u);
-          double oo = xi * (g - lds64(rp + 8 * u));
-          oo = qdiv(oo, dx, rdx);
-          // zero inflow at +v*
-          const int un = vsg > 0 ? u - 1 : u + 1;
-          const double nb = un < NV ? lds64(rcu + 8 * un) : 0.0;
-          const double d = vsg > 0 ? g - nb : nb - g;
-          if (vsg != 0) oo = oo + d * vco;
-          oo = oo - lds64(s_M + 8 * u) * dc;
-          const double forcing = oo + lds64(s_xiM + 8 * u) * J;
-          out_hi[mm] = k1 * g - k2 * forcing;
-        }
-      }
-    }
-    __syncwarp();
-    pump(last_q + 1 + S);  // positions < pos(last row) are consumed
-    if (active) {
       double* row = gout + (size_t)i * NV;
 #pragma unroll
       for (int mm = 0; mm < CH; ++mm) {
-        __stcg(row + k + 8 * mm, out_lo[mm]);
-        __stcg(row + NV - 1 - k - 8 * mm, out_hi[mm]);
-      }
-    }
-    // row moments: fold, in-lane pairwise chain k, 8-way tree (mesh.py:95-133)
-    double bx = 0.0, bsq = 0.0;
-    if (active) {
-#pragma unroll
-      for (int mm = 0; mm < CH; ++mm) {
         const int c = k + 8 * mm, u = NV - 1 - c;
-        const double f = lds64(s_vx + 8 * c) * out_lo[mm] + lds64(s_vx + 8 * u) * out_hi[mm];
-        const double h = out_lo[mm] * out_lo[mm] + out_hi[mm] * out_hi[mm];
+        double lo, hi;
+        {  // lower half, xi < 0: x-upwind from row i+1; zero inflow at -v*
+          const double g = lds64(rcu + 8 * c);
+          double oo = lds64(s_vx + 8 * c) * (lds64(rn + 8 * c) - g);
+          oo = qdiv(oo, dx, rdx);
+          const int cn = up ? c - 1 : c + 1;
+          const double nb = cn >= 0 ? lds64(rcu + 8 * cn) : 0.0;
+          oo = oo + (g - nb) * svco;
+          oo = oo - lds64(s_M + 8 * c) * dc;
+          const double forcing = oo + lds64(s_xiM + 8 * c) * J;
+          lo = k1 * g - k2 * forcing;
+        }
+        {  // upper half, xi > 0: x-upwind from row i-1; zero inflow at +v*
+          const double g = lds64(rcu + 8 * u);
+          double oo = lds64(s_vx + 8 * u) * (g - lds64(rp + 8 * u));
+          oo = qdiv(oo, dx, rdx);
+          const int un = up ? u - 1 : u + 1;
+          const double nb = un < NV ? lds64(rcu + 8 * un) : 0.0;
+          oo = oo + (g - nb) * svco;
+          oo = oo - lds64(s_M + 8 * u) * dc;
+          const double forcing = oo + lds64(s_xiM + 8 * u) * J;
+          hi = k1 * g - k2 * forcing;
+        }
+        __stcg(row + c, lo);
+        __stcg(row + u, hi);
+        // row moments: fold (lo + mirror), in-lane pairwise chain k
+        const double f = lds64(s_vx + 8 * c) * lo + lds64(s_vx + 8 * u) * hi;
+        const double h = lo * lo + hi * hi;
         bx = mm == 0 ? f : bx + f;
         bsq = mm == 0 ? h : bsq + h;
       }
     }
+    __syncwarp();
+    pump(last_q + 1 + S);  // positions < pos(last row) are consumed
     bx = bx + __shfl_xor_sync(FULL, bx, 1);
     bx = bx + __shfl_xor_sync(FULL, bx, 2);
     bx = bx + __shfl_xor_sync(FULL, bx, 4);
@@ -1134,8 +1145,16 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   long long c0 = prof ? clock64() : 0, c1;
   for (int s = 0; s < nst; ++s) {
     const int ph = s < n0 ? 0 : 1;
-    if constexpr (G != 0)
-      micro_phase_g8<G, S>(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg, ring_w, mbar_w, qbase);
+    if constexpr (G != 0) {
+      const int nkk = __ldcg(v.nk);
+      const int q0 = (int)(((long long)wg * nkk) / nwg), q1 = (int)(((long long)(wg + 1) * nkk) / nwg);
+      if (q0 < q1) {
+        if (nkk == nx)
+          micro_phase_g8<G, S, true>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w, qbase);
+        else
+          micro_phase_g8<G, S, false>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w, qbase);
+      }
+    }
     else if constexpr (T != 0)
       micro_phase_tma<T, S>(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg, ring_w, mbar_w, qbase);
     else
@@ -1356,7 +1375,8 @@ cudaError_t launch_lift(const LiftArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
-  const size_t smem = (sizeof(PwPlan) + 15) / 16 * 16 + (MAX_LEAF + MAX_NODE) * 8;
+  // slice_field's block_pairwise2 keeps two reductions in flight
+  const size_t smem = (sizeof(PwPlan) + 15) / 16 * 16 + 2 * (MAX_LEAF + MAX_NODE) * 8;
   cudaError_t e =
       cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1367,7 +1387,7 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   switch (a.m.nv) {
     case 64: return launch_T<2, 12, 4, 128>(a, C, st);   // G8 layout, 4 warps
-    case 128: return launch_T<4, 11, 8, 128>(a, C, st);  // G8 layout, 4 warps
+    case 128: return launch_T<4, 10, 8, 128>(a, C, st);  // G8 layout, 4 warps
     case 256: return launch_T<8, 3, 0, 256>(a, C, st);
     case 512: return launch_T<16, 3, 0, 256>(a, C, st);
     default:
