@@ -61,6 +61,8 @@ struct FineArgs {
   int8_t* vsg;
   uint8_t *flip, *nza, *nzb, *kcn, *kin;
   int* klist;
+  int* kpos;             // [B*nx] row-stream end after each listed row
+  int* kstream;          // [B*3nx] row id of each row-stream position
   int* nk;               // [B]
   int* abort_;           // [B]
   Status* status;

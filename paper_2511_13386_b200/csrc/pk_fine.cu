@@ -91,6 +91,8 @@ struct SliceView {
   double *fl, *sq, *fl_w, *sq_w;
   int8_t* vsg;
   int* klist;
+  int* kpos;
+  int* kstream;
   int* nk;
   int* abort_;
   double* ga;
@@ -102,7 +104,7 @@ struct SliceView {
 // first NLOC_DK / NLOC_BK only)
 constexpr int NLOC_D = 13;
 constexpr int NLOC_B = 7;
-constexpr int NLOC_DK = 7;
+constexpr int NLOC_DK = 5;
 constexpr int NLOC_BK = 2;
 
 __device__ __forceinline__ void bind_shared(SliceView& v, const FineArgs& a, int b) {
@@ -116,6 +118,8 @@ __device__ __forceinline__ void bind_shared(SliceView& v, const FineArgs& a, int
   v.vco = a.vco + o;
   v.vsg = a.vsg + o;
   v.klist = a.klist + o;
+  v.kpos = a.kpos + o;
+  v.kstream = a.kstream + 3 * o;
   v.nk = a.nk + b;
   v.abort_ = a.abort_ + b;
   v.ga = a.ga + o * a.m.nv;
@@ -139,6 +143,7 @@ __device__ __forceinline__ void bind_local(SliceView& v, const FineArgs& a, int 
     double* sq = nullptr;
     double** d[NLOC_D] = {&v.rho, &v.E, &v.Eprev, &v.J, &fl, &v.tA, &v.tB,
                           &sq, &v.tC, &v.tD, &v.tE, &v.bm, &v.blift};
+    // all-kinetic mode keeps only rho, E, E_prev, J and the moments on chip
     for (int k = 0; k < NLOC_D; ++k) *d[k] = k < nd ? p + (size_t)k * nx : nullptr;
     uint8_t* q = reinterpret_cast<uint8_t*>(p + (size_t)nd * nx);
     uint8_t** e[NLOC_B] = {&v.kc, &v.ki, &v.flip, &v.nza, &v.nzb, &v.kcn, &v.kin};
@@ -477,6 +482,26 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     if (v.ki[i]) v.klist[pre++] = i;
   if (tid == 0) *v.nk = total;
   __syncthreads();
+  // row-stream positions for the producer/consumer micro phase: entry p needs
+  // rows i-1, i, i+1; the rows not already needed by entry p-1 are
+  // min(3, i_p - i_{p-1}); kpos[p] = inclusive scan (stream end after p)
+  {
+    const int pe = (total + nt - 1) / nt;
+    const int a0 = min(total, tid * pe), a1 = min(total, a0 + pe);
+    int c = 0;
+    for (int q = a0; q < a1; ++q) c += q == 0 ? 3 : min(3, v.klist[q] - v.klist[q - 1]);
+    int pre2;
+    block_excl_scan(c, &pre2, sm.misc + 1);
+    for (int q = a0; q < a1; ++q) {
+      const int i = v.klist[q];
+      const int nn = q == 0 ? 3 : min(3, i - v.klist[q - 1]);
+      pre2 += nn;
+      v.kpos[q] = pre2;
+      // the stream's row ids: entry q adds rows i+2-nn .. i+1 (unwrapped)
+      for (int t = 0; t < nn; ++t) v.kstream[pre2 - nn + t] = i + 2 - nn + t;
+    }
+  }
+  __syncthreads();
   return true;
 }
 
@@ -501,17 +526,15 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
     } else {
       r = rho + cflu * (v.J[i] - v.J[ip]);
     }
-    v.tA[i] = r;
+    v.rho[i] = r;  // in place: each rho_i update reads only its own rho_i
   }
   __syncthreads();
-  // rho <- new density; the old E becomes E_prev (pointer rotation)
-  double* t = v.rho;
-  v.rho = v.tA;
-  v.tA = t;
-  t = v.Eprev;
+  // the new field is solved in place in the E_prev buffer; the old E becomes
+  // E_prev (pointer rotation)
+  double* t = v.Eprev;
   v.Eprev = v.E;
   v.E = t;
-  if (!slice_field(m, v.rho, v.rb, v.tB, v.E, a.rtol, a.exact_scan, sm,
+  if (!slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, sm,
                    (a.prof && v.b == 0) ? a.prof + 8 : nullptr)) {
     if (tid == 0) set_status(a.status, PK_ERR_SOLVABILITY, v.b, step);
     return false;
@@ -723,8 +746,24 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   };
   auto pump = [&](int q_limit) {
     if (DENSE) {
+      // all pending rows in ONE instruction, one lane per row: a bulk copy
+      // costs ~185 cycles of issue per thread, lanes overlap (~52 per extra)
       const int lim = min(q_limit, q_end);
-      for (; st.q_prod < lim; ++st.q_prod) issue(st.q_prod, p0 - 1 + st.q_prod);
+      const int n = lim - st.q_prod;
+      if (n > 0 && lane < n) {
+        const int q = st.q_prod + lane;
+        const uint32_t Q = qbase + (uint32_t)q;
+        const uint32_t slot = Q % S;
+        const uint32_t mb = s_mbar + 8 * slot;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(s_ring + slot * (RS * 8)),
+            "l"(gin + (size_t)wrap(p0 - 1 + q, nx) * NV), "r"(bytes), "r"(mb)
+            : "memory");
+      }
+      if (n > 0) st.q_prod = lim;
       return;
     }
     while (st.q_prod < q_limit) {
@@ -881,6 +920,242 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   qbase += (uint32_t)st.q_prod;
 }
 
+// ---------------------------------------------------------------------------
+// Micro phase, producer/consumer pipeline with the GS layout (nv = 64 SEG:
+// 64, 128, 256).
+//
+// One producer warp per CTA streams the rows this CTA needs (each fetched
+// once; i-1, i, i+1 of every listed row, deduplicated) into a CTA-wide TMA
+// ring: `full[slot]` completes when a row has landed, `done[op]` when a
+// consumer warp has finished an operation, which is what allows a slot to be
+// refilled.  Consumer warps take operations round-robin; an operation is
+// 4/SEG listed rows, each served by 8 SEG lanes.  Lane (k, seg) owns terms
+// m = 4 seg .. 4 seg + 3 of pairwise chain k of the velocity fold (columns
+// k + 8m and their mirrors nv-1-k-8m): 8 values, velocity constants in
+// registers, 3 shared-memory reads per value, and the chain passes between
+// segments in numpy's order with one shuffle hop per segment.
+template <int SEG>
+struct GS {
+  static constexpr int NV = 64 * SEG;   // velocities
+  static constexpr int LPR = 8 * SEG;   // lanes per row
+  static constexpr int RPO = 4 / SEG;   // rows per operation
+  static constexpr int RS = NV + 8;     // ring row stride (doubles): 64 B pad
+};
+
+// velocity constants of a lane's 8 columns; xi M is recomputed as
+// fl(vx * M), which is exactly how the host formed it (mesh.py:167)
+template <int SEG>
+struct GSConsts {
+  uint32_t s_vx, s_M, s_xiM;  // shared-memory addresses of the constant rows
+  __device__ void load(const Smem& sm, int) {
+    s_vx = smem_u32(sm.vx);
+    s_M = smem_u32(sm.M);
+    s_xiM = smem_u32(sm.xiM);
+  }
+};
+
+__device__ __forceinline__ void mbar_wait_u32(uint32_t mb, uint32_t par) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(mb), "r"(par)
+        : "memory");
+  } while (!ok);
+}
+
+template <int SEG, int R>
+__device__ void micro_phase_pc(const FineArgs& a, const SliceView& v, int ph, const double* gin,
+                               double* gout, int e0, int e1, bool dense, int nc, double* ring,
+                               uint64_t* full, uint64_t* done, uint32_t& qbase, uint32_t& obase,
+                               const GSConsts<SEG>& C) {
+  using L = GS<SEG>;
+  constexpr int NV = L::NV, RPO = L::RPO, RS = L::RS, Q = R;
+  const MeshDev& m = a.m;
+  const int nx = m.nx;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nent = e1 - e0;
+  const int nops = (nent + RPO - 1) / RPO;
+  const int kp0 = dense ? 0 : __ldcg(v.kpos + e0);
+  const int nstream = nent <= 0 ? 0 : (dense ? nent + 2 : __ldcg(v.kpos + e1 - 1) - kp0 + 3);
+  const int ngrp = (nstream + 7) >> 3;  // rows travel in groups of 8 (one barrier per group)
+  constexpr int NG = R / 8;
+  const uint32_t s_ring = smem_u32(ring), s_full = smem_u32(full), s_done = smem_u32(done);
+  constexpr uint32_t bytes = NV * 8;
+
+  if (nent > 0 && warp == nc) {
+    // ---------------- producer warp ----------------
+    // eight lanes issue one padded row each per group: a bulk copy costs
+    // ~185 cycles of issue per thread, so rows are issued eight at a time
+    if (lane == 0) fence_proxy_async_global();  // rows written by the generic proxy
+    __syncwarp();
+    const int i0 = dense ? e0 : __ldcg(v.klist + e0);
+    int pw = e0;
+    int jw = 0;  // next operation whose completion has not been observed
+    for (int g = 0; g < ngrp; ++g) {
+      const uint32_t G = (qbase >> 3) + (uint32_t)g;
+      if (g >= NG) {
+        // the group's previous occupant (positions up to x) is free once every
+        // operation up to its last reader is done; operations run on
+        // different warps and finish out of order, so wait for all of them
+        const int x = (g - NG) * 8 + 7;
+        int plast;
+        if (dense) {
+          plast = min(e0 + x, e1 - 1);
+        } else {
+          // position of row i-1 of entry p is kpos[p] - kpos[e0]
+          while (pw + 1 < e1 && __ldcg(v.kpos + pw + 1) - kp0 <= x) ++pw;
+          plast = pw;
+        }
+        const int jl = (plast - e0) / RPO;
+        for (; jw <= jl; ++jw) {
+          const uint32_t J = obase + (uint32_t)jw;
+          mbar_wait_u32(s_done + 8 * (J % Q), (J / Q) & 1);
+        }
+      }
+      const int nrows = min(8, nstream - 8 * g);
+      const uint32_t mb = s_full + 8 * (G % NG);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                     "r"(bytes * nrows)
+                     : "memory");
+      __syncwarp();
+      if (lane < nrows) {
+        const int q = 8 * g + lane;
+        const int row = dense ? e0 - 1 + q : (q < 3 ? i0 - 1 + q : __ldcg(v.kstream + kp0 + q - 3));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(s_ring + ((G % NG) * 8 + lane) * (RS * 8)),
+            "l"(gin + (size_t)wrap(row, nx) * NV), "r"(bytes), "r"(mb)
+            : "memory");
+      }
+    }
+  } else if (nent > 0 && warp < nc) {
+    // ---------------- consumers ----------------
+    const int k = lane & 7, seg = (lane >> 3) % SEG, grp = lane / L::LPR;
+    const double dx = m.dx, rdx = m.rdx, dv3 = m.dv3;
+    const PhaseDev& P = a.ph[ph];
+    const size_t o = (size_t)v.b * nx;
+    // coefficients of the next 32/RPO operations of this warp, one entry per lane
+    double c_vco = 0, c_dco = 0, c_J = 0, c_k1 = 0, c_k2 = 0;
+    int c_row = 0, c_pos = 0;
+    int jb = -1 << 30;  // first operation of the loaded batch
+    constexpr int OPB = 32 / RPO;
+    for (int j = warp; j < nops; j += nc) {
+      const int jj = (j - warp) / nc;  // this warp's operation ordinal
+      if (jj - jb >= OPB) {
+        jb = jj;
+        const int pl = e0 + (warp + (jb + lane / RPO) * nc) * RPO + lane % RPO;
+        if (pl < e1) {
+          const int r = dense ? pl : __ldcg(v.klist + pl);
+          const int sg = __ldcg(v.vsg + r);
+          const double vco = __ldcg(v.vco + r);
+          // signed E-upwind factor: (g - g_nb) * (+-vco) reproduces both of
+          // the reference's forms bitwise (kinetic.py:176-187); 0 when E == 0
+          c_vco = sg > 0 ? vco : (sg < 0 ? -vco : 0.0);
+          c_dco = __ldcg(v.dco + r);
+          c_J = __ldcg(v.gJ + r);
+          c_k1 = __ldg(P.k1 + o + r);
+          c_k2 = __ldg(P.k2 + o + r);
+          c_row = sg > 0 ? r : -1 - r;  // velocity-neighbour side in the sign
+          c_pos = dense ? pl - e0 : __ldcg(v.kpos + pl) - kp0;
+        }
+      }
+      const int src = (jj - jb) * RPO + grp;
+      const int p = e0 + j * RPO + grp;
+      const bool active = p < e1;
+      const int rsg = __shfl_sync(FULL, c_row, src);
+      const int pos = __shfl_sync(FULL, c_pos, src);
+      const double svco = __shfl_sync(FULL, c_vco, src);
+      const double dc = __shfl_sync(FULL, c_dco, src);
+      const double Jv = __shfl_sync(FULL, c_J, src);
+      const double k1 = __shfl_sync(FULL, c_k1, src);
+      const double k2 = __shfl_sync(FULL, c_k2, src);
+      const bool up = rsg >= 0;
+      const int i = up ? rsg : -1 - rsg;
+      double f[4], h[4];
+      if (active) {
+        uint32_t ra[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const uint32_t Qp = qbase + (uint32_t)(pos + d), G = Qp >> 3;
+          mbar_wait_u32(s_full + 8 * (G % NG), (G / NG) & 1);
+          ra[d] = s_ring + ((G % NG) * 8 + (Qp & 7)) * (RS * 8);
+        }
+        const uint32_t rp = ra[0], rc = ra[1], rn = ra[2];
+        double* row = gout + (size_t)i * NV;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int c = k + 8 * (4 * seg + t), u = NV - 1 - c;
+          double lo, hi, xl, xh;
+          {  // lower half, xi < 0: x-upwind from row i+1; zero inflow at -v*
+            const double g = lds64(rc + 8 * c);
+            xl = lds64(C.s_vx + 8 * c);
+            double oo = xl * (lds64(rn + 8 * c) - g);
+            oo = qdiv(oo, dx, rdx);
+            const int cn = up ? c - 1 : c + 1;
+            const double nb = cn >= 0 ? lds64(rc + 8 * cn) : 0.0;
+            oo = oo + (g - nb) * svco;
+            oo = oo - lds64(C.s_M + 8 * c) * dc;
+            const double forcing = oo + lds64(C.s_xiM + 8 * c) * Jv;
+            lo = k1 * g - k2 * forcing;
+          }
+          {  // upper half, xi > 0: x-upwind from row i-1; zero inflow at +v*
+            const double g = lds64(rc + 8 * u);
+            xh = lds64(C.s_vx + 8 * u);
+            double oo = xh * (g - lds64(rp + 8 * u));
+            oo = qdiv(oo, dx, rdx);
+            const int un = up ? u - 1 : u + 1;
+            const double nb = un < NV ? lds64(rc + 8 * un) : 0.0;
+            oo = oo + (g - nb) * svco;
+            oo = oo - lds64(C.s_M + 8 * u) * dc;
+            const double forcing = oo + lds64(C.s_xiM + 8 * u) * Jv;
+            hi = k1 * g - k2 * forcing;
+          }
+          __stcg(row + c, lo);
+          __stcg(row + u, hi);
+          f[t] = xl * lo + xh * hi;  // fold of xi g' (mesh.py:95-109)
+          h[t] = lo * lo + hi * hi;              // fold of g'^2
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) f[t] = h[t] = 0.0;
+      }
+      __syncwarp();
+      if (lane == 0) {  // this operation's ring rows are consumed
+        const uint32_t J = obase + (uint32_t)j;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_done + 8 * (J % Q))
+                     : "memory");
+      }
+      // pairwise chain k in numpy's order, passed segment to segment
+      double bx = ((f[0] + f[1]) + f[2]) + f[3];
+      double bq = ((h[0] + h[1]) + h[2]) + h[3];
+#pragma unroll
+      for (int s2 = 1; s2 < SEG; ++s2) {
+        const double ix = __shfl_up_sync(FULL, bx, 8);
+        const double iq = __shfl_up_sync(FULL, bq, 8);
+        if (seg == s2) {
+          bx = (((ix + f[0]) + f[1]) + f[2]) + f[3];
+          bq = (((iq + h[0]) + h[1]) + h[2]) + h[3];
+        }
+      }
+      bx = bx + __shfl_xor_sync(FULL, bx, 1);
+      bx = bx + __shfl_xor_sync(FULL, bx, 2);
+      bx = bx + __shfl_xor_sync(FULL, bx, 4);
+      bq = bq + __shfl_xor_sync(FULL, bq, 1);
+      bq = bq + __shfl_xor_sync(FULL, bq, 2);
+      bq = bq + __shfl_xor_sync(FULL, bq, 4);
+      if (active && k == 0 && seg == SEG - 1) {
+        v.fl_w[i] = bx * dv3;
+        v.sq_w[i] = bq * dv3;
+      }
+    }
+  }
+  qbase += (uint32_t)(8 * ngrp);
+  obase += (uint32_t)nops;
+}
+
 // Micro phase, generic layout (any nv <= 256, no TMA): direct row loads.
 __device__ void micro_phase_gen(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                 const double* gin, double* gout, int wg, int nwg) {
@@ -968,8 +1243,8 @@ __device__ bool lift_scalars(const FineArgs& a, const SliceView& v, const Smem& 
   const bool higher = a.lift_order == 2 && a.time_elim == 1;
   // temporaries: J_c in tA, D1(J_c) in tB (leader-local in every layout),
   // R in the global scratch tC (once per window)
-  double* Jc = v.tA;
-  double* d1 = v.tB;
+  double* Jc = a.tA + (size_t)v.b * nx;   // global scratch: once per window
+  double* d1 = a.tB + (size_t)v.b * nx;
   double* R = a.tC + (size_t)v.b * nx;
   for (int i = tid; i < nx; i += nt) {
     const int ip = wrap(i - 1, nx);
@@ -1012,7 +1287,9 @@ __device__ __forceinline__ void cluster_barrier(int C) {
 
 template <int T, int S, int G, int NT>
 __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
-  constexpr int RSN = G != 0 ? 16 * G + 8 : 32 * T;  // ring row stride (doubles)
+  // ring row stride (doubles); G > 0: per-warp G8 rings, G < 0: CTA-wide
+  // producer/consumer ring of the GS layout with SEG = -G
+  constexpr int RSN = G > 0 ? 16 * G + 8 : (G < 0 ? 64 * (-G) + 8 : 32 * T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
@@ -1035,7 +1312,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   {
     unsigned char* p = smem_raw;
     mbar = reinterpret_cast<uint64_t*>(p);
-    p += 64 * 8;
+    p += 128 * 8;
     sm.plan = reinterpret_cast<PwPlan*>(p);
     p += (sizeof(PwPlan) + 15) / 16 * 16;
     sm.vx = reinterpret_cast<double*>(p); p += nv * 8;
@@ -1048,7 +1325,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     if (T == 0) p += (size_t)nwpc * nv * 8;  // generic-layout row scratch
     if (T != 0) {
       ring = reinterpret_cast<double*>(p);
-      p += (size_t)nwpc * S * RSN * 8;
+      p += (size_t)(G < 0 ? 1 : nwpc) * S * RSN * 8;
     }
     if (a.local_smem) sm_loc = reinterpret_cast<double*>(p);  // same offset in every CTA
   }
@@ -1062,7 +1339,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       sm.xiM[j] = m.xiM[j];
       sm.w2[j] = m.w2[j];
     }
-    if (T != 0 && threadIdx.x < nwpc * S) mbar_init(mbar + threadIdx.x, 1);
+    if (T != 0 && threadIdx.x < (G < 0 ? 2 * S : nwpc * S)) mbar_init(mbar + threadIdx.x, 1);
     if (T != 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1082,8 +1359,10 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   auto nzf = [&](int s) { return ((s + (nst & 1)) & 1) ? v.nzb : v.nza; };
   int* abort_flag = v.abort_;
   const size_t o = (size_t)b * nx;
-  uint32_t qbase = 0;
-  double* ring_w = ring ? ring + (size_t)warp * S * RSN : nullptr;
+  uint32_t qbase = 0, obase = 0;
+  GSConsts<G < 0 ? -G : 1> gsc;
+  if constexpr (G < 0) gsc.load(sm, threadIdx.x & 31);
+  double* ring_w = ring ? ring + (size_t)(G < 0 ? 0 : warp) * S * RSN : nullptr;
   uint64_t* mbar_w = mbar + warp * S;
 
   // ---- prologue ----
@@ -1101,7 +1380,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     }
     if (tid == 0) *abort_flag = 0;
     __syncthreads();
-    bool ok = slice_field(m, v.rho, v.rb, v.tA, v.E, a.rtol, a.exact_scan, sm);
+    bool ok = slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, sm);
     if (!ok) {
       if (tid == 0) {
         set_status(a.status, PK_ERR_SOLVABILITY, b, 0);
@@ -1145,7 +1424,12 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   long long c0 = prof ? clock64() : 0, c1;
   for (int s = 0; s < nst; ++s) {
     const int ph = s < n0 ? 0 : 1;
-    if constexpr (G != 0) {
+    if constexpr (G < 0) {
+      const int nkk = __ldcg(v.nk);
+      const int e0 = (int)(((long long)crank * nkk) / C), e1 = (int)(((long long)(crank + 1) * nkk) / C);
+      micro_phase_pc<-G, S>(a, v, ph, buf(s), buf(s + 1), e0, e1, nkk == nx, nwpc - 1, ring, mbar,
+                            mbar + S, qbase, obase, gsc);
+    } else if constexpr (G > 0) {
       const int nkk = __ldcg(v.nk);
       const int q0 = (int)(((long long)wg * nkk) / nwg), q1 = (int)(((long long)(wg + 1) * nkk) / nwg);
       if (q0 < q1) {
@@ -1308,9 +1592,10 @@ __global__ void __launch_bounds__(256) field_kernel(const FieldArgs a) {
 constexpr int kThreads = 256;
 
 static size_t base_smem(int nv, int T, int S, int G, int NT) {
-  size_t s = 64 * 8 + (sizeof(PwPlan) + 15) / 16 * 16 + 4 * (size_t)nv * 8 +
+  size_t s = 128 * 8 + (sizeof(PwPlan) + 15) / 16 * 16 + 4 * (size_t)nv * 8 +
              2 * (MAX_LEAF + MAX_NODE) * 8 + 64 * 4;
   if (T == 0) s += (NT / 32) * (size_t)nv * 8;
+  else if (G < 0) s += (size_t)S * (nv + 8) * 8;
   else s += (size_t)(NT / 32) * S * (G != 0 ? nv + 8 : nv) * 8;
   return s;
 }
@@ -1386,9 +1671,10 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
 
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   switch (a.m.nv) {
-    case 64: return launch_T<2, 12, 4, 128>(a, C, st);   // G8 layout, 4 warps
-    case 128: return launch_T<4, 10, 8, 128>(a, C, st);  // G8 layout, 4 warps
-    case 256: return launch_T<8, 3, 0, 256>(a, C, st);
+    // producer/consumer GS pipeline: 7 consumer warps + 1 producer warp
+    case 64: return launch_T<2, 16, 4, 128>(a, C, st);   // G8 per-warp rings, 4 warps
+    case 128: return launch_T<4, 14, 8, 128>(a, C, st);  // G8 per-warp rings, 4 warps
+    case 256: return launch_T<8, 20, -4, 256>(a, C, st);
     case 512: return launch_T<16, 3, 0, 256>(a, C, st);
     default:
       if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
