@@ -66,6 +66,7 @@ typedef struct pk_phase {
   const double* kappa1;  /* [B*nx]  exp(-dt/eps_i**2)               kinetic.py:141-145 */
   const double* kappa2;  /* [B*nx]  eps_i * -expm1(-dt/eps_i**2) */
   const double* cmac;    /* [B*nx]  dt / (eps_i * dx)               kinetic.py:240 */
+  const double* cmac_scalar; /* [B] cmac when uniform in x (constant eps), else NaN */
 } pk_phase;
 
 /* Hybrid options (hybrid.py:45-55) and thresholds (adaptation.py:80-90). */

@@ -35,6 +35,7 @@ class PkPhase(C.Structure):
     _fields_ = [
         ("nsteps", C.c_void_p), ("dt", C.c_void_p), ("cflu", C.c_void_p),
         ("kappa1", C.c_void_p), ("kappa2", C.c_void_p), ("cmac", C.c_void_p),
+        ("cmac_scalar", C.c_void_p),
     ]
 
 

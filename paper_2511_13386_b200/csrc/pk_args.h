@@ -30,6 +30,7 @@ struct PhaseDev {
   const double* k1;     // [B*nx] exp(-dt/eps_i^2)          (kinetic.py:141-145)
   const double* k2;     // [B*nx] eps_i * -expm1(-dt/eps_i^2)
   const double* cmac;   // [B*nx] dt / (eps_i * dx)         (kinetic.py:240)
+  const double* cmacs;  // [B] the common value when uniform in x, else NaN
 };
 
 struct FineArgs {

@@ -62,6 +62,30 @@ __device__ __forceinline__ double warp_leaf(F x, int off, int n, int lane) {
   return r;
 }
 
+// One pairwise leaf per group of eight lanes (four leaves per warp at once).
+// `act`: this group has a leaf.  Same bits in the eight lanes of a group.
+template <class F>
+__device__ __forceinline__ double group_leaf(F x, int off, int n, bool act) {
+  const int k = threadIdx.x & 7;
+  double r = 0.0, seq = -0.0;
+  int full = 0;
+  if (act) {
+    if (n < 8) {
+      for (int i = 0; i < n; ++i) seq = seq + x(off + i);
+    } else {
+      full = n - (n % 8);
+      r = x(off + k);
+      for (int i = 8; i < full; i += 8) r = r + x(off + i + k);
+    }
+  }
+  r = r + __shfl_xor_sync(FULL, r, 1);
+  r = r + __shfl_xor_sync(FULL, r, 2);
+  r = r + __shfl_xor_sync(FULL, r, 4);
+  if (act && n >= 8)
+    for (int i = full; i < n; ++i) r = r + x(off + i);
+  return (act && n < 8) ? seq : r;
+}
+
 // Block-wide pairwise sum following a plan.  `scratch` is shared memory of at
 // least nleaf + nnode doubles.  Every thread of the block must call it; every
 // thread gets the result.
@@ -69,9 +93,11 @@ template <class F>
 __device__ double block_pairwise(F x, const PwPlan& P, double* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarp = blockDim.x >> 5;
-  for (int l = warp; l < P.nleaf; l += nwarp) {
-    double v = warp_leaf(x, P.leaf_off[l], P.leaf_len[l], lane);
-    if (lane == 0) scratch[l] = v;
+  for (int l0 = 4 * warp; l0 < P.nleaf; l0 += 4 * nwarp) {
+    const int l = l0 + (lane >> 3);
+    const bool act = l < P.nleaf;
+    const double v = group_leaf(x, act ? P.leaf_off[l] : 0, act ? P.leaf_len[l] : 0, act);
+    if (act && (lane & 7) == 0) scratch[l] = v;
   }
   __syncthreads();
   int start = 0;
@@ -88,36 +114,76 @@ __device__ double block_pairwise(F x, const PwPlan& P, double* scratch) {
   return res;
 }
 
+// Two pairwise sums over the same plan in one sweep (defect and scale of
+// poisson.py:42-43).  `scratch` holds 2 (nleaf + nnode) doubles.
+template <class F1, class F2>
+__device__ void block_pairwise2(F1 x1, F2 x2, const PwPlan& P, double* scratch, double& r1,
+                                double& r2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarp = blockDim.x >> 5;
+  const int W = P.nleaf + P.nnode;
+  for (int l0 = 4 * warp; l0 < P.nleaf; l0 += 4 * nwarp) {
+    const int l = l0 + (lane >> 3);
+    const bool act = l < P.nleaf;
+    const int off = act ? P.leaf_off[l] : 0, n = act ? P.leaf_len[l] : 0;
+    const double v1 = group_leaf(x1, off, n, act);
+    const double v2 = group_leaf(x2, off, n, act);
+    if (act && (lane & 7) == 0) {
+      scratch[l] = v1;
+      scratch[W + l] = v2;
+    }
+  }
+  __syncthreads();
+  int start = 0;
+  for (int lev = 0; lev < P.nlevel; ++lev) {
+    const int end = P.level_end[lev];
+    for (int j = start + threadIdx.x; j < end; j += blockDim.x) {
+      scratch[P.nleaf + j] = scratch[P.node_a[j]] + scratch[P.node_b[j]];
+      scratch[W + P.nleaf + j] = scratch[W + P.node_a[j]] + scratch[W + P.node_b[j]];
+    }
+    __syncthreads();
+    start = end;
+  }
+  const int root = P.nnode == 0 ? 0 : P.nleaf + P.nnode - 1;
+  r1 = scratch[root];
+  r2 = scratch[W + root];
+  __syncthreads();
+}
+
 // Sequential prefix sum (np.cumsum order) of src into dst by thread 0 of the
-// block.  The operands are software-pipelined through registers (the next
-// block of 16 is loaded before the current block's adds and stores), so the
+// block.  Operands are software-pipelined through two alternating register
+// blocks (the next block is loaded while the current one is summed), so the
 // only serial dependency is the add chain itself.  Other threads return.
 template <class FS, class FD>
 __device__ __forceinline__ void warp_cumsum(FS src, FD dst, int n) {
   if (threadIdx.x != 0) return;
-  constexpr int K = 16;
+  constexpr int K = 8;
   double acc = -0.0;  // -0.0 + t == t bitwise: out[0] = src[0]
-  const int nk = n - n % K;
-  double cur[K];
-  if (nk > 0) {
+  const int n2 = n - n % (2 * K);
+  double A[K], Bv[K];
+  if (n2 > 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) cur[k] = src(k);
+    for (int k = 0; k < K; ++k) A[k] = src(k);
   }
-  for (int i = 0; i < nk; i += K) {
-    double nxt[K];
-    if (i + K < nk) {
+  for (int i = 0; i < n2; i += 2 * K) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) nxt[k] = src(i + K + k);
+    for (int k = 0; k < K; ++k) Bv[k] = src(i + K + k);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      acc = acc + A[k];
+      dst(i + k, acc);
+    }
+    if (i + 2 * K < n2) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) A[k] = src(i + 2 * K + k);
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      acc = acc + cur[k];
-      dst(i + k, acc);
+      acc = acc + Bv[k];
+      dst(i + K + k, acc);
     }
-#pragma unroll
-    for (int k = 0; k < K; ++k) cur[k] = nxt[k];
   }
-  for (int i = nk; i < n; ++i) {
+  for (int i = n2; i < n; ++i) {
     acc = acc + src(i);
     dst(i, acc);
   }
@@ -134,34 +200,43 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
 }
 
 // warp_cumsum for operands that live in shared memory: explicit LDS/STS
-// (generic accesses cost ~2.5x the chain latency).  Thread 0 only.
+// (generic accesses cost ~2x the chain latency).  dst may alias src: every
+// operand is loaded before its slot is overwritten.  Two register blocks
+// alternate (ping-pong, no register copies): block A's adds run while block
+// B's loads are in flight, so the only serial dependency is the add chain.
+// Keep the operand a plain load: an extra DADD per element (e.g. a fused
+// subtrahend) doubles the cost (tools/cumsum_bench.cu).  Thread 0 only.
 __device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int n) {
   if (threadIdx.x != 0) return;
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(src);
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-  constexpr int K = 16;
+  constexpr int K = 8;
   double acc = -0.0;
-  const int nk = n - n % K;
-  double cur[K];
-  if (nk > 0) {
+  const int n2 = n - n % (2 * K);
+  double A[K], Bv[K];
+  if (n2 > 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) cur[k] = lds64(s + 8 * k);
+    for (int k = 0; k < K; ++k) A[k] = lds64(s + 8 * k);
   }
-  for (int i = 0; i < nk; i += K) {
-    double nxt[K];
-    if (i + K < nk) {
+  for (int i = 0; i < n2; i += 2 * K) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) nxt[k] = lds64(s + 8 * (i + K + k));
+    for (int k = 0; k < K; ++k) Bv[k] = lds64(s + 8 * (i + K + k));
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      acc = acc + A[k];
+      sts64(d + 8 * (i + k), acc);
+    }
+    if (i + 2 * K < n2) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) A[k] = lds64(s + 8 * (i + 2 * K + k));
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      acc = acc + cur[k];
-      sts64(d + 8 * (i + k), acc);
+      acc = acc + Bv[k];
+      sts64(d + 8 * (i + K + k), acc);
     }
-#pragma unroll
-    for (int k = 0; k < K; ++k) cur[k] = nxt[k];
   }
-  for (int i = nk; i < n; ++i) {
+  for (int i = n2; i < n; ++i) {
     acc = acc + lds64(s + 8 * i);
     sts64(d + 8 * i, acc);
   }

@@ -200,45 +200,12 @@ __device__ __forceinline__ double stencil_at(const double* v, int i, int nx, con
   return acc * m.sts[p - 1];
 }
 
-// Two pairwise sums over the same plan in one sweep (defect and scale of
-// poisson.py:42-43).
-template <class F1, class F2>
-__device__ void block_pairwise2(F1 x1, F2 x2, const PwPlan& P, double* scratch, double& r1,
-                                double& r2) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarp = blockDim.x >> 5;
-  const int W = P.nleaf + P.nnode;
-  for (int l = warp; l < P.nleaf; l += nwarp) {
-    const double v1 = warp_leaf(x1, P.leaf_off[l], P.leaf_len[l], lane);
-    const double v2 = warp_leaf(x2, P.leaf_off[l], P.leaf_len[l], lane);
-    if (lane == 0) {
-      scratch[l] = v1;
-      scratch[W + l] = v2;
-    }
-  }
-  __syncthreads();
-  int start = 0;
-  for (int lev = 0; lev < P.nlevel; ++lev) {
-    const int end = P.level_end[lev];
-    for (int j = start + threadIdx.x; j < end; j += blockDim.x) {
-      scratch[P.nleaf + j] = scratch[P.node_a[j]] + scratch[P.node_b[j]];
-      scratch[W + P.nleaf + j] = scratch[W + P.node_a[j]] + scratch[W + P.node_b[j]];
-    }
-    __syncthreads();
-    start = end;
-  }
-  const int root = P.nnode == 0 ? 0 : P.nleaf + P.nnode - 1;
-  r1 = scratch[root];
-  r2 = scratch[W + root];
-  __syncthreads();
-}
-
 // E_out = solve_field(rho); false on a solvability violation.
 // poisson.py:41-54: src=(rho-rb)dx; defect=sum(src); guard; src-=defect/nx;
 // E=cumsum(src); E-=mean(E).
 __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, double* src,
-                            double* E_out, double rtol, int exact_scan, const Smem& sm,
-                            long long* dbg = nullptr) {
+                            double* E_out, double rtol, int exact_scan, bool on_chip,
+                            const Smem& sm, long long* dbg = nullptr) {
   const int nx = m.nx;
   long long c0 = dbg ? clock64() : 0;
 #define PK_TICK(k)                         \
@@ -263,7 +230,7 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
   __syncthreads();
   PK_TICK(2)
   if (exact_scan) {
-    if (__isShared(src) && __isShared(E_out))
+    if (on_chip)  // src and E_out in this CTA's shared memory
       smem_cumsum(src, E_out, nx);
     else
       warp_cumsum([&](int i) { return src[i]; }, [&](int i, double v) { E_out[i] = v; }, nx);
@@ -514,6 +481,7 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
   const PhaseDev& P = a.ph[ph];
   const size_t o = (size_t)v.b * nx;
   const double cflu = P.cflu[v.b];
+  const double cs = P.cmacs ? P.cmacs[v.b] : __longlong_as_double(0x7ff8000000000000LL);
   for (int i = tid; i < nx; i += nt) {
     const int ip = wrap(i - 1, nx);
     const double rho = v.rho[i];
@@ -521,7 +489,8 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
     if (v.kc[i]) {
       const double fi = v.ki[i] ? v.fl[i] : 0.0;
       const double fp = v.ki[ip] ? v.fl[ip] : 0.0;
-      const double ci = P.cmac[o + i], cp = P.cmac[o + ip];
+      // constant eps: one scalar, no per-row loads (bitwise the same value)
+      const double ci = cs == cs ? cs : P.cmac[o + i], cp = cs == cs ? cs : P.cmac[o + ip];
       r = (ci == cp) ? rho - ci * (fi - fp) : rho - (ci * fi - cp * fp);
     } else {
       r = rho + cflu * (v.J[i] - v.J[ip]);
@@ -534,7 +503,7 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
   double* t = v.Eprev;
   v.Eprev = v.E;
   v.E = t;
-  if (!slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, sm,
+  if (!slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, a.local_smem != 0, sm,
                    (a.prof && v.b == 0) ? a.prof + 8 : nullptr)) {
     if (tid == 0) set_status(a.status, PK_ERR_SOLVABILITY, v.b, step);
     return false;
@@ -1380,7 +1349,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     }
     if (tid == 0) *abort_flag = 0;
     __syncthreads();
-    bool ok = slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, sm);
+    bool ok = slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, a.local_smem != 0, sm);
     if (!ok) {
       if (tid == 0) {
         set_status(a.status, PK_ERR_SOLVABILITY, b, 0);
@@ -1471,6 +1440,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   if (prof) {
     for (int k = 0; k < 5; ++k) a.prof[k] += tp[k];
     a.prof[5] += nst;
+    a.prof[15] = a.local_smem;
   }
   // ---- epilogue: leader-local state back to the caller's arrays ----
   if (leader && sm_loc) {
@@ -1581,7 +1551,7 @@ __global__ void __launch_bounds__(256) field_kernel(const FieldArgs a) {
   __syncthreads();
   const size_t o = (size_t)blockIdx.x * a.m.nx;
   if (!slice_field(a.m, a.rho + o, a.rho_bar[blockIdx.x], a.src + o, a.E + o, a.rtol,
-                   a.exact_scan, sm)) {
+                   a.exact_scan, false, sm)) {
     if (threadIdx.x == 0) set_status(a.status, PK_ERR_SOLVABILITY, blockIdx.x, 0);
   }
 }

@@ -10,31 +10,39 @@
 
 namespace pk {
 
-__device__ static bool chain_field(const MeshDev& m, const double* rho, double rb, double* src,
-                                   double* E, double rtol, int exact_scan, const PwPlan& plan,
-                                   double* red) {
+constexpr int CHAIN_NT = 256;
+constexpr int CHAIN_MAXPER = (MAX_LEAF * 128 + CHAIN_NT - 1) / CHAIN_NT;  // cells per thread
+
+// Field of rho into E, up to the zero-mean shift: returns false on a
+// solvability violation, else E holds cumsum(src - defect/nx) and `mean` its
+// mean, so the field is E[i] - mean (poisson.py:41-54; the subtraction is
+// applied where E is read, with the same rounding).  E doubles as src.
+__device__ static bool chain_field(const MeshDev& m, const double* rho, double rb, double* E,
+                                   double rtol, int exact_scan, const PwPlan& plan, double* red,
+                                   double& mean) {
   const int nx = m.nx;
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = (rho[i] - rb) * m.dx;
+  for (int i = threadIdx.x; i < nx; i += CHAIN_NT) E[i] = (rho[i] - rb) * m.dx;
   __syncthreads();
-  const double defect = block_pairwise([&](int i) { return src[i]; }, plan, red);
-  const double scale = block_pairwise([&](int i) { return fabs(rho[i]); }, plan, red) * m.dx;
+  double defect, abssum;
+  block_pairwise2([&](int i) { return E[i]; }, [&](int i) { return fabs(rho[i]); }, plan, red,
+                  defect, abssum);
+  const double scale = abssum * m.dx;
   if (fabs(defect) > rtol * fmax(scale, 2.2250738585072014e-308)) return false;
   const double corr = defect / (double)nx;
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = src[i] - corr;
+  for (int i = threadIdx.x; i < nx; i += CHAIN_NT) E[i] = E[i] - corr;
   __syncthreads();
-  if (exact_scan) {
-    warp_cumsum([&](int i) { return src[i]; }, [&](int i, double v) { E[i] = v; }, nx);
-  } else {
-    block_scan_fast([&](int i) { return src[i]; }, [&](int i, double v) { E[i] = v; }, nx, red);
-  }
+  if (exact_scan)
+    smem_cumsum(E, E, nx);
+  else
+    block_scan_fast([&](int i) { return E[i]; }, [&](int i, double v) { E[i] = v; }, nx, red);
   __syncthreads();
-  const double mean = block_pairwise([&](int i) { return E[i]; }, plan, red) / (double)nx;
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) E[i] = E[i] - mean;
-  __syncthreads();
+  mean = block_pairwise([&](int i) { return E[i]; }, plan, red) / (double)nx;
   return true;
 }
 
-__global__ void __launch_bounds__(512) chain_kernel(const ChainArgs a) {
+// PER: cells per thread (nx <= PER * CHAIN_NT), so the new-rho registers stay unspilled.
+template <int PER>
+__global__ void __launch_bounds__(CHAIN_NT) chain_kernel(const ChainArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const MeshDev& m = a.m;
   const int nx = m.nx;
@@ -43,18 +51,18 @@ __global__ void __launch_bounds__(512) chain_kernel(const ChainArgs a) {
   double* base = reinterpret_cast<double*>(smem_raw + (sizeof(PwPlan) + 15) / 16 * 16);
   double* rho = base;
   double* E = rho + nx;
-  double* J = E + nx;
-  double* src = J + nx;
-  double* red = src + nx;
+  double* red = E + nx;
   {
     const int* s = reinterpret_cast<const int*>(m.plan_x);
     int* d = reinterpret_cast<int*>(plan);
-    for (int i = threadIdx.x; i < (int)(sizeof(PwPlan) / 4); i += blockDim.x) d[i] = s[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(PwPlan) / 4); i += CHAIN_NT) d[i] = s[i];
   }
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) rho[i] = a.rho_in[(size_t)c * nx + i];
+  for (int i = threadIdx.x; i < nx; i += CHAIN_NT) rho[i] = a.rho_in[(size_t)c * nx + i];
   __syncthreads();
   const double rb = a.rho_bar[c];
+  const double dx = m.dx;
   bool have_E = false;
+  double mean = 0.0;  // pending zero-mean shift of E (x - 0.0 == x bitwise)
   for (int w = 0; w < a.nwin; ++w) {
     const size_t cw = (size_t)c * a.nwin + w;
     const int nfull = a.nfull[cw];
@@ -62,9 +70,10 @@ __global__ void __launch_bounds__(512) chain_kernel(const ChainArgs a) {
     if (nfull > 0 || rem > 0.0) {
       if (w == 0 && a.E_in) {
         // fluid_step: the caller guarantees E matches rho (fluid.py:69-71)
-        for (int i = threadIdx.x; i < nx; i += blockDim.x) E[i] = a.E_in[(size_t)c * nx + i];
+        for (int i = threadIdx.x; i < nx; i += CHAIN_NT) E[i] = a.E_in[(size_t)c * nx + i];
+        mean = 0.0;
         __syncthreads();
-      } else if (!chain_field(m, rho, rb, src, E, a.rtol, a.exact_scan, *plan, red)) {
+      } else if (!chain_field(m, rho, rb, E, a.rtol, a.exact_scan, *plan, red, mean)) {
         // fluid_propagate: the field is refreshed from rho on entry (fluid.py:111-113)
         if (threadIdx.x == 0) set_status(a.status, PK_ERR_SOLVABILITY, c, w);
         return;
@@ -73,47 +82,66 @@ __global__ void __launch_bounds__(512) chain_kernel(const ChainArgs a) {
       const int nstep = nfull + (rem > 0.0 ? 1 : 0);
       for (int s = 0; s < nstep; ++s) {
         const double cflu = s < nfull ? a.cflu_full[cw] : a.cflu_rem[cw];
-        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-          const int in_ = i + 1 == nx ? 0 : i + 1;
-          const double r = rho[i], rn = rho[in_];
-          J[i] = (rn - r) / m.dx - E[i] * 0.5 * (r + rn);   // fluid.py:51-52
+        // rho_i += cflu (J_{i+1/2} - J_{i-1/2})   (fluid.py:51-57); each J is
+        // formed twice (once per neighbour) with identical operands and bits.
+        double nr[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int i = threadIdx.x + k * CHAIN_NT;
+          if (i < nx) {
+            const int ip = i == 0 ? nx - 1 : i - 1, in_ = i + 1 == nx ? 0 : i + 1;
+            const double r = rho[i], rp = rho[ip], rn = rho[in_];
+            const double Ji = (rn - r) / dx - (E[i] - mean) * 0.5 * (r + rn);
+            const double Jp = (r - rp) / dx - (E[ip] - mean) * 0.5 * (rp + r);
+            nr[k] = r + cflu * (Ji - Jp);
+          }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-          const int ip = i == 0 ? nx - 1 : i - 1;
-          rho[i] = rho[i] + cflu * (J[i] - J[ip]);           // fluid.py:57
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int i = threadIdx.x + k * CHAIN_NT;
+          if (i < nx) rho[i] = nr[k];
         }
         __syncthreads();
-        if (!chain_field(m, rho, rb, src, E, a.rtol, a.exact_scan, *plan, red)) {
+        if (!chain_field(m, rho, rb, E, a.rtol, a.exact_scan, *plan, red, mean)) {
           if (threadIdx.x == 0) set_status(a.status, PK_ERR_SOLVABILITY, c, w);
           return;
         }
       }
     }
     if (a.gout)
-      for (int i = threadIdx.x; i < nx; i += blockDim.x) a.gout[cw * nx + i] = rho[i];
+      for (int i = threadIdx.x; i < nx; i += CHAIN_NT) a.gout[cw * nx + i] = rho[i];
     if (a.delta) {
       // new_row[n] = coarse.rho + deltas[n]   (parareal.py:281)
-      for (int i = threadIdx.x; i < nx; i += blockDim.x) rho[i] = rho[i] + a.delta[cw * nx + i];
+      for (int i = threadIdx.x; i < nx; i += CHAIN_NT) rho[i] = rho[i] + a.delta[cw * nx + i];
     }
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) a.out[cw * nx + i] = rho[i];
+    for (int i = threadIdx.x; i < nx; i += CHAIN_NT) a.out[cw * nx + i] = rho[i];
     __syncthreads();
   }
   if (a.Eout && have_E)
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) a.Eout[(size_t)c * nx + i] = E[i];
+    for (int i = threadIdx.x; i < nx; i += CHAIN_NT) a.Eout[(size_t)c * nx + i] = E[i] - mean;
 }
 
 size_t chain_smem_bytes(int nx) {
-  return (sizeof(PwPlan) + 15) / 16 * 16 + (size_t)4 * nx * 8 + (MAX_LEAF + MAX_NODE) * 8;
+  return (sizeof(PwPlan) + 15) / 16 * 16 + (size_t)2 * nx * 8 + 2 * (MAX_LEAF + MAX_NODE) * 8;
 }
 
 cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st) {
   const size_t smem = chain_smem_bytes(a.m.nx);
-  cudaError_t e =
-      cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  chain_kernel<<<a.nchain, 512, smem, st>>>(a);
-  return cudaGetLastError();
+  const int per = (a.m.nx + CHAIN_NT - 1) / CHAIN_NT;
+  auto go = [&](auto kern) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<a.nchain, CHAIN_NT, smem, st>>>(a);
+    return cudaGetLastError();
+  };
+  if (per <= 2) return go(chain_kernel<2>);
+  if (per <= 4) return go(chain_kernel<4>);
+  if (per <= 8) return go(chain_kernel<8>);
+  if (per <= 16) return go(chain_kernel<16>);
+  if (per <= 32) return go(chain_kernel<32>);
+  return go(chain_kernel<CHAIN_MAXPER>);
 }
 
 // Delta = F - G (parareal.py:429) and the finiteness check of parareal.py:267-269.

@@ -53,6 +53,7 @@ class Phase:
     k1: np.ndarray       # [B, nx]
     k2: np.ndarray       # [B, nx]
     cmac: np.ndarray     # [B, nx]
+    cmac_scalar: np.ndarray = None  # [B]: the common cmac when uniform in x, else NaN
 
 
 def eps_rows(eps, nx: int) -> np.ndarray:
@@ -99,7 +100,8 @@ def make_phase(mesh: PhaseMesh, eps_list, dt_list, nsteps_list) -> Phase:
         k2[b] = per_value(e, lambda v: relaxation_coefficients(dt, v)[1])
         cm[b] = per_value(e, lambda v: dt / (v * dx))
         cflu[b] = m2 * (dt / dx)
-    return Phase(np.asarray(nsteps_list, dtype=np.int32), dts, cflu, k1, k2, cm)
+    cs = np.array([row[0] if (row == row[0]).all() else np.nan for row in cm])
+    return Phase(np.asarray(nsteps_list, dtype=np.int32), dts, cflu, k1, k2, cm, cs)
 
 
 @dataclass
@@ -223,10 +225,11 @@ class Device:
         torch = _torch()
         dev = dict(
             nsteps=self.t(ph.nsteps.astype(np.int32)), dt=self.t(ph.dt), cflu=self.t(ph.cflu),
-            k1=self.t(ph.k1), k2=self.t(ph.k2), cmac=self.t(ph.cmac))
+            k1=self.t(ph.k1), k2=self.t(ph.k2), cmac=self.t(ph.cmac), cs=self.t(ph.cmac_scalar))
         s = _native.PkPhase()
         s.nsteps, s.dt, s.cflu = _ptr(dev["nsteps"]), _ptr(dev["dt"]), _ptr(dev["cflu"])
         s.kappa1, s.kappa2, s.cmac = _ptr(dev["k1"]), _ptr(dev["k2"]), _ptr(dev["cmac"])
+        s.cmac_scalar = _ptr(dev["cs"])
         del torch
         return s, dev
 

@@ -59,6 +59,7 @@ def main():
               % tuple(int(x) // ns for x in c[:5]))
         print("   field cycles/step: src %d, pairwise2 %d, corr %d, cumsum %d, mean %d, sub %d"
               % tuple(int(x) // ns for x in c[8:14]))
+        print("   slice vectors in shared memory:", bool(c[15]))
 
 
 if __name__ == "__main__":
