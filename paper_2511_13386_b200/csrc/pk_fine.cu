@@ -667,7 +667,7 @@ __device__ void micro_phase_tma(const FineArgs& a, const SliceView& v, const Sme
 // Every operand (row i, its x-neighbours, the velocity neighbours) is read
 // from the TMA ring in shared memory; ring rows are padded by 64 B so the
 // four groups of a warp hit distinct bank halves.
-template <int CH, int S, bool DENSE>
+template <int CH, int S, bool DENSE, bool SQ>
 __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                const double* gin, double* gout, int p0, int p1, double* ring,
                                uint64_t* mbar, uint32_t& qbase) {
@@ -840,10 +840,11 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
 #pragma unroll
       for (int mm = 0; mm < CH; ++mm) {
         const int c = k + 8 * mm, u = NV - 1 - c;
+        const double vxc = lds64(s_vx + 8 * c), vxu = lds64(s_vx + 8 * u);
         double lo, hi;
         {  // lower half, xi < 0: x-upwind from row i+1; zero inflow at -v*
           const double g = lds64(rcu + 8 * c);
-          double oo = lds64(s_vx + 8 * c) * (lds64(rn + 8 * c) - g);
+          double oo = vxc * (lds64(rn + 8 * c) - g);
           oo = qdiv(oo, dx, rdx);
           const int cn = up ? c - 1 : c + 1;
           const double nb = cn >= 0 ? lds64(rcu + 8 * cn) : 0.0;
@@ -854,7 +855,7 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
         }
         {  // upper half, xi > 0: x-upwind from row i-1; zero inflow at +v*
           const double g = lds64(rcu + 8 * u);
-          double oo = lds64(s_vx + 8 * u) * (g - lds64(rp + 8 * u));
+          double oo = vxu * (g - lds64(rp + 8 * u));
           oo = qdiv(oo, dx, rdx);
           const int un = up ? u - 1 : u + 1;
           const double nb = un < NV ? lds64(rcu + 8 * un) : 0.0;
@@ -866,10 +867,12 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
         __stcg(row + c, lo);
         __stcg(row + u, hi);
         // row moments: fold (lo + mirror), in-lane pairwise chain k
-        const double f = lds64(s_vx + 8 * c) * lo + lds64(s_vx + 8 * u) * hi;
-        const double h = lo * lo + hi * hi;
+        const double f = vxc * lo + vxu * hi;
         bx = mm == 0 ? f : bx + f;
-        bsq = mm == 0 ? h : bsq + h;
+        if (SQ) {
+          const double h = lo * lo + hi * hi;
+          bsq = mm == 0 ? h : bsq + h;
+        }
       }
     }
     __syncwarp();
@@ -877,12 +880,14 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
     bx = bx + __shfl_xor_sync(FULL, bx, 1);
     bx = bx + __shfl_xor_sync(FULL, bx, 2);
     bx = bx + __shfl_xor_sync(FULL, bx, 4);
-    bsq = bsq + __shfl_xor_sync(FULL, bsq, 1);
-    bsq = bsq + __shfl_xor_sync(FULL, bsq, 2);
-    bsq = bsq + __shfl_xor_sync(FULL, bsq, 4);
+    if (SQ) {
+      bsq = bsq + __shfl_xor_sync(FULL, bsq, 1);
+      bsq = bsq + __shfl_xor_sync(FULL, bsq, 2);
+      bsq = bsq + __shfl_xor_sync(FULL, bsq, 4);
+    }
     if (active && k == 0) {
       v.fl_w[i] = bx * dv3;
-      v.sq_w[i] = bsq * dv3;
+      if (SQ) v.sq_w[i] = bsq * dv3;
     }
     p += nent;
   }
@@ -1402,10 +1407,16 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       const int nkk = __ldcg(v.nk);
       const int q0 = (int)(((long long)wg * nkk) / nwg), q1 = (int)(((long long)(wg + 1) * nkk) / nwg);
       if (q0 < q1) {
-        if (nkk == nx)
-          micro_phase_g8<G, S, true>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w, qbase);
+        // the |g|^2 row moment feeds only the adaptation labels
+        if (nkk == nx && !a.adaptation)
+          micro_phase_g8<G, S, true, false>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w,
+                                            qbase);
+        else if (nkk == nx)
+          micro_phase_g8<G, S, true, true>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w,
+                                           qbase);
         else
-          micro_phase_g8<G, S, false>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w, qbase);
+          micro_phase_g8<G, S, false, true>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w,
+                                            qbase);
       }
     }
     else if constexpr (T != 0)
