@@ -200,6 +200,77 @@ __device__ __forceinline__ double stencil_at(const double* v, int i, int nx, con
   return acc * m.sts[p - 1];
 }
 
+// stencil_at on a register window w[o] = v[i + o - 3] (same terms, same order)
+__device__ __forceinline__ double stencil_reg(const double (&w)[7], const MeshDev& m, int p) {
+  double acc = 0.0;
+#pragma unroll
+  for (int o = 0; o < 7; ++o) {
+    const double c = m.stc[p - 1][o];
+    if (c != 0.0) acc = acc + c * w[o];
+  }
+  return acc * m.sts[p - 1];
+}
+
+// np.cumsum of a global-memory vector staged through shared memory: thread 0
+// streams 2 KB chunks with TMA bulk copies (4-slot ring, three chunks ahead,
+// so the L2 latency hides behind the add chain) and runs the ping-pong LDS
+// chain over each chunk; results go to dst with plain stores.  dst may alias
+// src: chunk c+4 is fetched after elements < (c+1)*256 are written.  n even
+// (bulk copies move 16-byte granules).  Thread 0 only.
+constexpr int STAGE_CH = 256, STAGE_NS = 4;
+
+__device__ void staged_cumsum(const double* src, double* dst, int n, double* stage, uint64_t* mb) {
+  if (threadIdx.x != 0) return;
+  const int nch = (n + STAGE_CH - 1) / STAGE_CH;
+  for (int s = 0; s < STAGE_NS; ++s) mbar_init(mb + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  fence_proxy_async_global();  // src was written by the generic proxy
+  auto issue = [&](int c) {
+    const uint32_t bytes = (uint32_t)min(STAGE_CH, n - c * STAGE_CH) * 8u;
+    uint64_t* m = mb + c % STAGE_NS;
+    mbar_expect_tx(m, bytes);
+    bulk_g2s(stage + (c % STAGE_NS) * STAGE_CH, src + (size_t)c * STAGE_CH, bytes, m);
+  };
+  for (int c = 0; c < min(STAGE_NS, nch); ++c) issue(c);
+  double acc = -0.0;
+  for (int c = 0; c < nch; ++c) {
+    mbar_wait(mb + c % STAGE_NS, (uint32_t)(c / STAGE_NS) & 1u);
+    const uint32_t s0 = smem_u32(stage + (c % STAGE_NS) * STAGE_CH);
+    double* d = dst + (size_t)c * STAGE_CH;
+    const int len = min(STAGE_CH, n - c * STAGE_CH);
+    constexpr int K = 8;
+    const int n2 = len - len % (2 * K);
+    double A[K], Bv[K];
+    if (n2 > 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) A[k] = lds64(s0 + 8 * k);
+    }
+    for (int i = 0; i < n2; i += 2 * K) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) Bv[k] = lds64(s0 + 8 * (i + K + k));
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        acc = acc + A[k];
+        d[i + k] = acc;
+      }
+      if (i + 2 * K < n2) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) A[k] = lds64(s0 + 8 * (i + 2 * K + k));
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        acc = acc + Bv[k];
+        d[i + K + k] = acc;
+      }
+    }
+    for (int i = n2; i < len; ++i) {
+      acc = acc + lds64(s0 + 8 * i);
+      d[i] = acc;
+    }
+    if (c + STAGE_NS < nch) issue(c + STAGE_NS);  // slot consumed (values in registers)
+  }
+}
+
 // E_out = solve_field(rho); false on a solvability violation.
 // poisson.py:41-54: src=(rho-rb)dx; defect=sum(src); guard; src-=defect/nx;
 // E=cumsum(src); E-=mean(E).
@@ -232,6 +303,8 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
   if (exact_scan) {
     if (on_chip)  // src and E_out in this CTA's shared memory
       smem_cumsum(src, E_out, nx);
+    else if (sm.stage && nx % 2 == 0)
+      staged_cumsum(src, E_out, nx, sm.stage, sm.smb);
     else
       warp_cumsum([&](int i) { return src[i]; }, [&](int i, double v) { E_out[i] = v; }, nx);
   } else {
@@ -281,6 +354,18 @@ __device__ int block_excl_scan(int v, int* out_prefix, int* sbuf) {
   return total;
 }
 
+// Unordered compaction: every lane of the warp calls it (same trip count);
+// lanes with f append i to list through one warp-aggregated shared atomic.
+__device__ __forceinline__ void list_append(bool f, int i, int* list, int* count) {
+  const unsigned bal = __ballot_sync(FULL, f);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31, lead = __ffs(bal) - 1;
+  int base = 0;
+  if (lane == lead) base = atomicAdd(count, __popc(bal));
+  base = __shfl_sync(FULL, base, lead);
+  if (f) list[base + __popc(bal & ((1u << lane) - 1u))] = i;
+}
+
 // ---------------------------------------------------------------------------
 // Slice phase: prepare step `s` (labels, flips, projection coefficients, row
 // list) from rho, E (start of step s), Eprev and the moments fl/sq of the
@@ -289,12 +374,19 @@ __device__ int block_excl_scan(int v, int* out_prefix, int* sbuf) {
 template <int T>
 __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& sm, double dt,
                              int moment_all, double* gin, double* gout, uint8_t* nzin,
-                             uint8_t* nzout, int step) {
+                             uint8_t* nzout, int step, long long* dbg = nullptr) {
+  long long c0 = dbg ? clock64() : 0;
+#define PK_PTICK(k)                        \
+  if (dbg && threadIdx.x == 0) {           \
+    const long long c1 = clock64();        \
+    dbg[k] += c1 - c0;                     \
+    c0 = c1;                               \
+  }
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
-  int* sflags = sm.misc;  // [0]: any flip, [1..32]: scan scratch
+  int* sflags = sm.misc;  // [0]: any flip, [1..32]: scan scratch, [40]/[41]: list sizes
 
   if (!a.adaptation) {
     // all-kinetic: J, and the projection/E-upwind coefficients from the
@@ -316,55 +408,171 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     return true;
   }
 
-  for (int i = tid; i < nx; i += nt) {
-    const double J = flux_J(v.rho[i], v.rho[wrap(i + 1, nx)], v.E[i], m.dx);
-    v.J[i] = J;
-    v.gJ[i] = J;
+  // The element loops below run over global memory when the slice vectors do
+  // not fit on chip (large nx): every operand of U iterations is loaded
+  // unconditionally first (restrict views, no load behind a branch), so the
+  // L2 round trips of consecutive iterations overlap.
+  const double* __restrict__ rho_ = v.rho;
+  const double* __restrict__ E_ = v.E;
+  const double* __restrict__ Ep_ = v.Eprev;
+  double* __restrict__ J_ = v.J;
+  double* __restrict__ gJ_ = v.gJ;
+  double* __restrict__ tA_ = v.tA;
+  double* __restrict__ tB_ = v.tB;
+  {
+    constexpr int U = 4;
+    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+      double r0[U], r1[U], e[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nx - 1);
+        r0[u] = rho_[i];
+        r1[u] = rho_[wrap(i + 1, nx)];
+        e[u] = E_[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nt;
+        if (i < nx) {
+          const double J = flux_J(r0[u], r1[u], e[u], m.dx);
+          J_[i] = J;
+          gJ_[i] = J;
+        }
+      }
+    }
   }
-  if (tid == 0) sflags[0] = 0;
+  if (tid == 0) {
+    sflags[0] = 0;
+    sflags[40] = 0;
+    sflags[41] = 0;
+  }
   __syncthreads();
+  PK_PTICK(0)
   // remainder indicator (adaptation.py:120-152) at cells
-  for (int i = tid; i < nx; i += nt) {
-    const int ip = wrap(i - 1, nx);
-    v.tA[i] = (v.E[i] - v.Eprev[i]) / dt;   // (E - E_prev)/dt
-    v.tB[i] = 0.5 * (v.J[ip] + v.J[i]);     // J_c
+  {
+    constexpr int U = 4;
+    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+      double e[U], ep[U], j0[U], j1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nx - 1);
+        e[u] = E_[i];
+        ep[u] = Ep_[i];
+        j0[u] = J_[wrap(i - 1, nx)];
+        j1[u] = J_[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nt;
+        if (i < nx) {
+          tA_[i] = (e[u] - ep[u]) / dt;  // (E - E_prev)/dt
+          tB_[i] = 0.5 * (j0[u] + j1[u]);  // J_c
+        }
+      }
+    }
   }
   __syncthreads();
-  const double three_rb = 3.0 * v.rb;
-  for (int i = tid; i < nx; i += nt) {
-    const int ip = wrap(i - 1, nx);
-    const double dtEc = 0.5 * (v.tA[ip] + v.tA[i]);
-    const double Ec = 0.5 * (v.E[ip] + v.E[i]);
-    const double d1J = stencil_at(v.tB, i, nx, m, 1);
-    const double d2J = stencil_at(v.tB, i, nx, m, 2);
-    const double d3J = stencil_at(v.tB, i, nx, m, 3);
-    const double d1r = stencil_at(v.rho, i, nx, m, 1);
-    const double rho = v.rho[i];
-    const double Jc = v.tB[i];
-    const double R = -d3J + Ec * d2J + (2.0 * rho - three_rb) * d1J + 2.0 * Jc * d1r - d1r * dtEc;
-    v.tC[i] = R;    // unscaled R (lift, higher_order)
-    v.tD[i] = d1J;  // D1(J_c) (lift drift)
-    const double Rs = a.rscale ? a.rscale[(size_t)v.b * nx + i] * R : R;
-    // perturbation indicator (adaptation.py:155-159) on the incoming g
-    const double sqp = (moment_all || v.ki[ip]) ? v.sq[ip] : 0.0;
-    const double sqi = (moment_all || v.ki[i]) ? v.sq[i] : 0.0;
-    const double gn = sqrt(0.5 * (sqp + sqi));
-    const bool fR = fabs(Rs) < a.delta0;
-    const bool fg = gn < a.eta0;
-    const bool fluid = a.combine_and ? (fR && fg) : (fR || fg);
-    v.kcn[i] = fluid ? 0 : 1;
+  {
+    const double three_rb = 3.0 * v.rb;
+    const double* __restrict__ sq_ = v.sq;
+    const uint8_t* __restrict__ ki_ = v.ki;
+    double* __restrict__ tC_ = v.tC;
+    double* __restrict__ tD_ = v.tD;
+    uint8_t* __restrict__ kcn_ = v.kcn;
+    const double* __restrict__ rsc = a.rscale ? a.rscale + (size_t)v.b * nx : nullptr;
+    constexpr int U = 2;
+    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+      double wB[U][7], wR[U][7], a0[U], a1[U], e0[U], e1[U], s0[U], s1[U], rs[U];
+      int k0[U], k1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nx - 1);
+        const int ip = wrap(i - 1, nx);
+#pragma unroll
+        for (int o = 0; o < 7; ++o) {
+          const int j = wrap(i + o - 3, nx);
+          wB[u][o] = tB_[j];
+          wR[u][o] = rho_[j];
+        }
+        a0[u] = tA_[ip];
+        a1[u] = tA_[i];
+        e0[u] = E_[ip];
+        e1[u] = E_[i];
+        s0[u] = sq_[ip];
+        s1[u] = sq_[i];
+        k0[u] = ki_[ip];
+        k1[u] = ki_[i];
+        rs[u] = rsc ? rsc[i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nt;
+        if (i < nx) {
+          const double dtEc = 0.5 * (a0[u] + a1[u]);
+          const double Ec = 0.5 * (e0[u] + e1[u]);
+          const double d1J = stencil_reg(wB[u], m, 1);
+          const double d2J = stencil_reg(wB[u], m, 2);
+          const double d3J = stencil_reg(wB[u], m, 3);
+          const double d1r = stencil_reg(wR[u], m, 1);
+          const double rho = wR[u][3];
+          const double Jc = wB[u][3];
+          const double R =
+              -d3J + Ec * d2J + (2.0 * rho - three_rb) * d1J + 2.0 * Jc * d1r - d1r * dtEc;
+          tC_[i] = R;    // unscaled R (lift, higher_order)
+          tD_[i] = d1J;  // D1(J_c) (lift drift)
+          const double Rs = rsc ? rs[u] * R : R;
+          // perturbation indicator (adaptation.py:155-159) on the incoming g
+          const double sqp = (moment_all || k0[u]) ? s0[u] : 0.0;
+          const double sqi = (moment_all || k1[u]) ? s1[u] : 0.0;
+          const double gn = sqrt(0.5 * (sqp + sqi));
+          const bool fR = fabs(Rs) < a.delta0;
+          const bool fg = gn < a.eta0;
+          const bool fluid = a.combine_and ? (fR && fg) : (fR || fg);
+          kcn_[i] = fluid ? 0 : 1;
+        }
+      }
+    }
   }
   __syncthreads();
+  PK_PTICK(1)
+  // flipped interfaces (F -> K) are listed (klist is free until the row list
+  // below), so the row work touches only them
   int anyflip = 0;
-  for (int i = tid; i < nx; i += nt) {
-    const uint8_t kin = v.kcn[i] | v.kcn[wrap(i + 1, nx)];
-    v.kin[i] = kin;
-    const uint8_t f = (kin && !v.ki[i]) ? 1 : 0;
-    v.flip[i] = f;
-    anyflip |= f;
+  {
+    const uint8_t* __restrict__ kcn_ = v.kcn;
+    const uint8_t* __restrict__ ki_ = v.ki;
+    uint8_t* __restrict__ kin_ = v.kin;
+    uint8_t* __restrict__ flip_ = v.flip;
+    constexpr int U = 4;
+    for (int i00 = 0; i00 < nx; i00 += U * nt) {  // uniform trip count (ballots inside)
+      int c0[U], c1[U], k[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i00 + u * nt + tid, nx - 1);
+        c0[u] = kcn_[i];
+        c1[u] = kcn_[wrap(i + 1, nx)];
+        k[u] = ki_[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i00 + u * nt + tid;
+        uint8_t f = 0;
+        if (i < nx) {
+          const uint8_t kin = (uint8_t)(c0[u] | c1[u]);
+          kin_[i] = kin;
+          f = (kin && !k[u]) ? 1 : 0;
+          flip_[i] = f;
+        }
+        anyflip |= f;
+        list_append(f != 0, i, v.klist, &sflags[40]);
+      }
+    }
   }
   if (anyflip) atomicOr(&sflags[0], 1);
   __syncthreads();
+  PK_PTICK(2)
+  const int nflip = sflags[40];
+  if (dbg && tid == 0) dbg[10] += nflip;
   if (sflags[0]) {
     if (a.reinit == 0) {
       if (a.lift_order != 1 && a.lift_order != 2) {
@@ -376,16 +584,16 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
         return false;
       }
       // lift scalars at the flipped interfaces (lifting.py:63-88); dE_dt = (E - E_prev)/dt
-      for (int i = tid; i < nx; i += nt) {
-        if (!v.flip[i]) continue;
+      for (int q = tid; q < nflip; q += nt) {
+        const int i = v.klist[q];
         const int in_ = wrap(i + 1, nx);
         const double dJ = 0.5 * (v.tD[i] + v.tD[in_]);
         v.tE[i] = dJ - v.E[i] * v.J[i];          // drift
         v.tA[i] = 0.5 * (v.tC[i] + v.tC[in_]);   // R_if
       }
       __syncthreads();
-      for (int i = warp; i < nx; i += nwarp) {
-        if (!v.flip[i]) continue;
+      for (int q = warp; q < nflip; q += nwarp) {
+        const int i = v.klist[q];
         LiftRow L;
         const size_t o = (size_t)v.b * nx + i;
         L.negJ = a.neg_eps[o] * v.J[i];
@@ -400,8 +608,8 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
         if (lane == 0) v.blift[i] = bx;
       }
     } else if (a.reinit == 1) {
-      for (int i = warp; i < nx; i += nwarp) {
-        if (!v.flip[i]) continue;
+      for (int q = warp; q < nflip; q += nwarp) {
+        const int i = v.klist[q];
         row_zero_store<T>(gin + (size_t)i * nv, lane, nv);
         if (lane == 0) v.blift[i] = 0.0;
       }
@@ -412,32 +620,95 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   }
   __syncthreads();
   // masked projection moment (hybrid.py:103-105) on the post-flip rows
-  for (int i = tid; i < nx; i += nt) {
-    const bool valid = moment_all || v.ki[i];
-    v.bm[i] = v.kin[i] ? (v.flip[i] ? v.blift[i] : (valid ? v.fl[i] : 0.0)) : 0.0;
-    if (!moment_all && v.flip[i]) nzin[i] = 1;
+  PK_PTICK(3)
+  {
+    uint8_t* __restrict__ ki_ = v.ki;
+    uint8_t* __restrict__ kc_ = v.kc;
+    const uint8_t* __restrict__ kin_ = v.kin;
+    const uint8_t* __restrict__ kcn_ = v.kcn;
+    const uint8_t* __restrict__ flip_ = v.flip;
+    const double* __restrict__ blift_ = v.blift;
+    const double* __restrict__ fl_ = v.fl;
+    double* __restrict__ bm_ = v.bm;
+    constexpr int U = 4;
+    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+      int k[U], kn[U], kcv[U], f[U];
+      double bl[U], fv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nx - 1);
+        k[u] = ki_[i];
+        kn[u] = kin_[i];
+        kcv[u] = kcn_[i];
+        f[u] = flip_[i];
+        bl[u] = blift_[i];
+        fv[u] = fl_[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nt;
+        if (i < nx) {
+          const bool valid = moment_all || k[u];
+          bm_[i] = kn[u] ? (f[u] ? bl[u] : (valid ? fv[u] : 0.0)) : 0.0;
+          if (!moment_all && f[u]) nzin[i] = 1;
+          kc_[i] = (uint8_t)kcv[u];
+          ki_[i] = (uint8_t)kn[u];
+        }
+      }
+    }
   }
   __syncthreads();
-  for (int i = tid; i < nx; i += nt) {
-    v.kc[i] = v.kcn[i];
-    v.ki[i] = v.kin[i];
-  }
-  __syncthreads();
+  PK_PTICK(4)
   // projection coefficient dc (kinetic.py:190-191) and E-upwind factor
   // max(E,0)/dvx or min(E,0)/dvx (kinetic.py:177-178); zero the output rows of
   // interfaces that are not kinetic this step but may hold data in the output
   // buffer (kinetic->fluid transitions, hybrid.py:166)
-  for (int i = tid; i < nx; i += nt) {
-    v.dco[i] = (v.bm[wrap(i + 1, nx)] - v.bm[wrap(i - 1, nx)]) / m.two_dx;
-    const double e = v.E[i];
-    v.vsg[i] = e > 0.0 ? 1 : (e < 0.0 ? -1 : 0);
-    v.vco[i] = e / m.dvx;
-    if (!v.ki[i] && nzout[i]) {
-      double* row = gout + (size_t)i * nv;
-      for (int j = 0; j < nv; ++j) row[j] = 0.0;
-      nzout[i] = 0;
+  {
+    const double* __restrict__ bm_ = v.bm;
+    const uint8_t* __restrict__ ki_ = v.ki;
+    double* __restrict__ dco_ = v.dco;
+    double* __restrict__ vco_ = v.vco;
+    int8_t* __restrict__ vsg_ = v.vsg;
+    uint8_t* __restrict__ nzo = nzout;
+    constexpr int U = 4;
+    for (int i00 = 0; i00 < nx; i00 += U * nt) {  // uniform trip count (ballots inside)
+      double b1[U], b0[U], e[U];
+      int k[U], nz[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i00 + u * nt + tid, nx - 1);
+        b1[u] = bm_[wrap(i + 1, nx)];
+        b0[u] = bm_[wrap(i - 1, nx)];
+        e[u] = E_[i];
+        k[u] = ki_[i];
+        nz[u] = nzo[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i00 + u * nt + tid;
+        bool z = false;
+        if (i < nx) {
+          dco_[i] = (b1[u] - b0[u]) / m.two_dx;
+          vsg_[i] = e[u] > 0.0 ? 1 : (e[u] < 0.0 ? -1 : 0);
+          vco_[i] = e[u] / m.dvx;
+          z = !k[u] && nz[u];
+          if (z) nzo[i] = 0;
+        }
+        // rows to zero are listed in kstream (free until the row stream below)
+        list_append(z, i, v.kstream, &sflags[41]);
+      }
     }
   }
+  __syncthreads();
+  PK_PTICK(5)
+  {
+    const int nz = sflags[41];
+    if (dbg && tid == 0) dbg[11] += nz;
+    for (int q = warp; q < nz; q += nwarp)
+      row_zero_store<T>(gout + (size_t)v.kstream[q] * nv, lane, nv);
+  }
+  __syncthreads();
+  PK_PTICK(6)
   // compacted kinetic-row list (order preserving)
   const int per = (nx + nt - 1) / nt;
   const int lo = min(nx, tid * per), hi = min(nx, lo + per);
@@ -448,7 +719,9 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   for (int i = lo; i < hi; ++i)
     if (v.ki[i]) v.klist[pre++] = i;
   if (tid == 0) *v.nk = total;
+  if (dbg && tid == 0) dbg[12] += total;
   __syncthreads();
+  PK_PTICK(7)
   // row-stream positions for the producer/consumer micro phase: entry p needs
   // rows i-1, i, i+1; the rows not already needed by entry p-1 are
   // min(3, i_p - i_{p-1}); kpos[p] = inclusive scan (stream end after p)
@@ -469,6 +742,8 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     }
   }
   __syncthreads();
+  PK_PTICK(8)
+#undef PK_PTICK
   return true;
 }
 
@@ -1265,6 +1540,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   // producer/consumer ring of the GS layout with SEG = -G
   constexpr int RSN = G > 0 ? 16 * G + 8 : (G < 0 ? 64 * (-G) + 8 : 32 * T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const long long t_kstart = a.prof ? clock64() : 0;
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
   int C = 1;
@@ -1302,6 +1578,8 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       p += (size_t)(G < 0 ? 1 : nwpc) * S * RSN * 8;
     }
     if (a.local_smem) sm_loc = reinterpret_cast<double*>(p);  // same offset in every CTA
+    sm.stage = a.local_smem ? nullptr : reinterpret_cast<double*>(p);
+    sm.smb = mbar + 120;  // slots past every ring's mbarriers
   }
   {
     const int* src = reinterpret_cast<const int*>(m.plan_x);
@@ -1396,6 +1674,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   const bool prof = a.prof && b == 0 && leader && threadIdx.x == 0;
   long long tp[6] = {0, 0, 0, 0, 0, 0};
   long long c0 = prof ? clock64() : 0, c1;
+  if (prof) a.prof[6] += c0 - t_kstart;  // prologue
   for (int s = 0; s < nst; ++s) {
     const int ph = s < n0 ? 0 : 1;
     if constexpr (G < 0) {
@@ -1439,7 +1718,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
         }
         const int phn = (s + 1) < n0 ? 0 : 1;
         ok = prepare_step<T>(a, v, sm, a.ph[phn].dt[b], 0, buf(s + 1), buf(s), nzf(s + 1),
-                             nzf(s), s + 1);
+                             nzf(s), s + 1, (a.prof && b == 0) ? a.prof + 16 : nullptr);
       }
       if (!ok && threadIdx.x == 0) *abort_flag = 1;
       if (prof) { c1 = clock64(); tp[3] += c1 - c0; c0 = c1; }
@@ -1590,7 +1869,7 @@ template <int T, int S, int G, int NT>
 static cudaError_t launch_T(FineArgs a, int C, cudaStream_t st) {
   const size_t base = base_smem(a.m.nv, T, S, G, NT);
   // slice vectors on chip when two CTAs still fit per SM
-  size_t smem = base;
+  size_t smem = base + STAGE_NS * STAGE_CH * 8;  // scan staging ring
   a.local_smem = 0;
   if (base + local_smem(a.m.nx, a.adaptation) <= 112 * 1024) {
     a.local_smem = 1;

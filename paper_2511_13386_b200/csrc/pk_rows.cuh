@@ -17,6 +17,8 @@ struct Smem {
   double* red;    // pairwise scratch (MAX_LEAF + MAX_NODE)
   double* wrow;   // generic rows: one nv-row per warp
   int* misc;      // small ints
+  double* stage = nullptr;  // scan staging ring (global-memory slice vectors), or null
+  uint64_t* smb = nullptr;  // its mbarriers
 };
 
 // ---------------------------------------------------------------------------
