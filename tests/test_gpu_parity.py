@@ -376,3 +376,37 @@ def test_invalid_reinit_raises_on_flip():
     with pytest.raises(ValueError):
         pk.hybrid_step(st, p, pk.Thresholds(1e-5, 1e-5), pk.HybridOptions(reinit="nearest"),
                        m, rb, field_rtol=1e-5)
+
+
+def test_cfg3_window2_guard_and_relaxed(gold):
+    """BASELINE cfg3 (eps(x) bump, delta0 = eta0 = 1e-3) window 2 of the first
+    parareal iteration through the drop-in API: coarse sweep over window 1,
+    lift restart, hybrid steps.  Under the reference's guard (rtol 1e-5) the
+    solvability check trips at the oracle's step; with the guard
+    relaxed to 1e-2 (explicit extension, same on both sides) the state after
+    600 steps -- masks, rho, E, E_prev, g -- is bitwise the oracle's."""
+    d = gold("eps_hybrid")
+    c = configs.cfg3()
+    m = c.mesh
+    th = pk.Thresholds(1e-3, 1e-3)
+    opts = pk.HybridOptions(adaptation=True)
+    cfg = pk.PararealConfig(eps=c.eps, t_final=1.0, ng=32, tol=1e-8, thresholds=th, options=opts)
+    E0 = pk.solve_field(c.rho, c.rho_bar, m, rtol=1e-5)
+    fluid_p, kin_p = pk.parareal.default_params(cfg, m, E0)
+    assert kin_p.dt == d["dt_f"] and fluid_p.dt == d["dt_c"]
+    mac = pk.fluid_propagate(pk.MacroState(c.rho, E0, 0.0), float(cfg.boundaries[1]), fluid_p, m,
+                             c.rho_bar, field_rtol=1e-5)
+    rho1 = mac.rho
+    assert eq(rho1, d["rho1"])
+    E1 = pk.solve_field(rho1, c.rho_bar, m, rtol=1e-5)
+    g1 = pk.lift(rho1, E1, c.eps, m, order=2, time_elim="leading", rho_bar=c.rho_bar)
+    st = pk.HybridState.initial(pk.MacroState(rho1, E1, 0.0), g1, m)
+    with pytest.raises(pk.SolvabilityViolation, match=f"step {int(d['guard_step'])}"):
+        pk.hybrid_propagate(st, 2000 * kin_p.dt, kin_p, th, opts, m, c.rho_bar, field_rtol=1e-5)
+    n = int(d["relaxed_steps"])
+    out = pk.hybrid_propagate(st, n * kin_p.dt, kin_p, th, opts, m, c.rho_bar,
+                              field_rtol=float(d["relaxed_rtol"]))
+    assert eq(out.labels.kinetic_cells, d["r_kc"]) and eq(out.labels.kinetic_ifaces, d["r_ki"])
+    assert eq(out.macro.rho, d["r_rho"]) and eq(out.macro.E, d["r_E"])
+    assert eq(out.E_prev, d["r_Eprev"])
+    assert digest(out.micro.g.reshape(m.nx, m.nv)) == str(d["r_g_digest"])

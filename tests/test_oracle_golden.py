@@ -184,3 +184,22 @@ def test_eps_profile_constant_reduces_to_scalar():
     a = O.hpropagate(st, 40.5 * dt, dt, 1e-3, 1e-2, 1e-2, O.HOpts(combine="and"), grid, rb, 1e-2)
     b = O.hpropagate(st, 40.5 * dt, dt, prof, 1e-2, 1e-2, O.HOpts(combine="and"), grid, rb, 1e-2)
     assert eq(a.rho, b.rho) and eq(a.g, b.g) and eq(a.kc, b.kc)
+
+
+def test_eps_hybrid_cfg3_window2(gold):
+    """eps(x) fixture (made by the oracle, tests/golden/make_eps_golden.py) is
+    reproducible: the rtol-1e-5 guard trips at the recorded step of cfg3's
+    window 2, and the relaxed-guard state after 600 steps matches."""
+    import sys
+
+    sys.path.insert(0, __import__("os").path.join(__import__("os").path.dirname(__file__), "golden"))
+    import make_eps_golden as M
+
+    d = gold("eps_hybrid")
+    g, eps, cfg, rb, dt_c, dt_f, rho1, E1, g1 = M.window2_start()
+    assert dt_f == d["dt_f"] and dt_c == d["dt_c"] and np.array_equal(rho1, d["rho1"])
+    st = O.restate.HState.start(rho1, E1, g1, 0.0)
+    for s in range(int(d["guard_step"])):
+        st = O.restate.hstep(st, dt_f, eps, cfg.delta0, cfg.eta0, cfg.opts, g, rb, cfg.rtol)
+    with pytest.raises(O.restate.OracleSolvability):
+        O.restate.hstep(st, dt_f, eps, cfg.delta0, cfg.eta0, cfg.opts, g, rb, cfg.rtol)

@@ -44,7 +44,9 @@ def cfg3(args):
     windows = sum(32 - k for k in range(res.iterations))
     nominal = windows * steps * c.mesh.nx * c.mesh.nv
     kf = np.asarray(res.kinetic_fraction, dtype=float)
-    return {"config": "cfg3: Nx=512, Nv=128, eps(x)=1e-3+0.5exp(-20(x-pi)^2), delta0=eta0=1e-3, "
+    mass = np.asarray(res.boundary_rho).sum(axis=1) * c.mesh.dx
+    drift = float(np.max(np.abs(mass - mass[0])) / abs(mass[0]))
+    return {"max_rel_mass_drift_boundary_rows": drift,"config": "cfg3: Nx=512, Nv=128, eps(x)=1e-3+0.5exp(-20(x-pi)^2), delta0=eta0=1e-3, "
                       "32 slices, T=1, tol 1e-8, reference dt",
             "status": res.status, "iterations": res.iterations, "err": [float(e) for e in res.ledger.err],
             "wall_s": wall, "fine_s": tm.fine_total, "correction_s": tm.correction_total,
@@ -129,8 +131,23 @@ def main():
     ap.add_argument("--k-max", type=int, default=50)
     ap.add_argument("--fine-steps", type=int, default=200)
     ap.add_argument("--coarse-steps", type=int, default=50)
+    ap.add_argument("--field-rtol", type=float, default=None,
+                    help="relax the adaptive solvability guard (reference: 1e-5)")
     a = ap.parse_args()
-    out = cfg3(a) if a.cfg == 3 else cfg4(a)
+    import paper_2511_13386_b200 as pk
+
+    if a.field_rtol is not None:
+        # explicit extension: the reference's module-level guard
+        # (parareal.py:45-52) relaxed for the whole run, reported in the output
+        pk.parareal.ADAPTIVE_FIELD_RTOL = a.field_rtol
+    t0 = time.perf_counter()
+    try:
+        out = cfg3(a) if a.cfg == 3 else cfg4(a)
+    except pk.SimulationError as e:  # the reference raises the same typed errors
+        out = {"config": f"cfg{a.cfg}", "status": "raised", "error": type(e).__name__,
+               "detail": str(e), "wall_s_until_raise": time.perf_counter() - t0}
+    out["field_rtol"] = pk.parareal.ADAPTIVE_FIELD_RTOL
+    out["field_rtol_is_reference"] = a.field_rtol is None
     print(json.dumps(out), flush=True)
 
 
