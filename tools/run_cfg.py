@@ -144,8 +144,13 @@ def main():
     try:
         out = cfg3(a) if a.cfg == 3 else cfg4(a)
     except pk.SimulationError as e:  # the reference raises the same typed errors
+        import traceback
+
+        frames = [f"{fr.name}:{fr.lineno}" for fr in traceback.extract_tb(e.__traceback__)
+                  if "paper_2511_13386_b200" in fr.filename]
         out = {"config": f"cfg{a.cfg}", "status": "raised", "error": type(e).__name__,
-               "detail": str(e), "wall_s_until_raise": time.perf_counter() - t0}
+               "detail": str(e), "raised_in": frames[-4:],
+               "wall_s_until_raise": time.perf_counter() - t0}
     out["field_rtol"] = pk.parareal.ADAPTIVE_FIELD_RTOL
     out["field_rtol_is_reference"] = a.field_rtol is None
     print(json.dumps(out), flush=True)
