@@ -371,7 +371,7 @@ __device__ __forceinline__ void list_append(bool f, int i, int* list, int* count
 // list) from rho, E (start of step s), Eprev and the moments fl/sq of the
 // rows stored in gin.  `moment_all`: moments are valid on every row
 // (prologue: user g) rather than only on the previous step's kinetic rows.
-template <int T>
+template <int T, bool AD>
 __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& sm, double dt,
                              int moment_all, double* gin, double* gout, uint8_t* nzin,
                              uint8_t* nzout, int step, long long* dbg = nullptr) {
@@ -388,7 +388,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   int* sflags = sm.misc;  // [0]: any flip, [1..32]: scan scratch, [40]/[41]: list sizes
 
-  if (!a.adaptation) {
+  if constexpr (!AD) {
     // all-kinetic: J, and the projection/E-upwind coefficients from the
     // unmasked moments (kinetic.py:177-178,190-191,221)
     for (int i = tid; i < nx; i += nt) {
@@ -1534,7 +1534,9 @@ __device__ __forceinline__ void cluster_barrier(int C) {
   }
 }
 
-template <int T, int S, int G, int NT>
+// AD: adaptation on (hybrid) or off (all-kinetic, compiled without the
+// labels / lifts / row lists of the hybrid slice phase)
+template <int T, int S, int G, int NT, bool AD>
 __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   // ring row stride (doubles); G > 0: per-warp G8 rings, G < 0: CTA-wide
   // producer/consumer ring of the GS layout with SEG = -G
@@ -1661,7 +1663,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   cluster_barrier(C);
   if (leader) {
     const double dt0 = (n0 > 0 ? a.ph[0].dt : a.ph[1].dt)[b];
-    if (!prepare_step<T>(a, v, sm, dt0, 1, buf(0), buf(1), nzf(0), nzf(1), 0)) {
+    if (!prepare_step<T, AD>(a, v, sm, dt0, 1, buf(0), buf(1), nzf(0), nzf(1), 0)) {
       if (threadIdx.x == 0) *abort_flag = 1;
     }
   }
@@ -1687,7 +1689,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       const int q0 = (int)(((long long)wg * nkk) / nwg), q1 = (int)(((long long)(wg + 1) * nkk) / nwg);
       if (q0 < q1) {
         // the |g|^2 row moment feeds only the adaptation labels
-        if (nkk == nx && !a.adaptation)
+        if constexpr (!AD)
           micro_phase_g8<G, S, true, false>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w,
                                             qbase);
         else if (nkk == nx)
@@ -1711,13 +1713,13 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       if (ok && s + 1 < nst) {
         // step s+1 reads buf(s+1) and writes buf(s+2) == buf(s); after step
         // s the rows of buf(s+1) hold data exactly on step s's kinetic rows.
-        if (a.adaptation) {
+        if (AD) {
           uint8_t* nzn = nzf(s + 1);
           for (int i = threadIdx.x; i < nx; i += blockDim.x) nzn[i] = v.ki[i];
           __syncthreads();
         }
         const int phn = (s + 1) < n0 ? 0 : 1;
-        ok = prepare_step<T>(a, v, sm, a.ph[phn].dt[b], 0, buf(s + 1), buf(s), nzf(s + 1),
+        ok = prepare_step<T, AD>(a, v, sm, a.ph[phn].dt[b], 0, buf(s + 1), buf(s), nzf(s + 1),
                              nzf(s), s + 1, (a.prof && b == 0) ? a.prof + 16 : nullptr);
       }
       if (!ok && threadIdx.x == 0) *abort_flag = 1;
@@ -1865,8 +1867,8 @@ static size_t local_smem(int nx, int adaptation) {
                     : (size_t)nx * (NLOC_DK * 8 + NLOC_BK) + 16;
 }
 
-template <int T, int S, int G, int NT>
-static cudaError_t launch_T(FineArgs a, int C, cudaStream_t st) {
+template <int T, int S, int G, int NT, bool AD>
+static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   const size_t base = base_smem(a.m.nv, T, S, G, NT);
   // slice vectors on chip when two CTAs still fit per SM
   size_t smem = base + STAGE_NS * STAGE_CH * 8;  // scan staging ring
@@ -1875,7 +1877,7 @@ static cudaError_t launch_T(FineArgs a, int C, cudaStream_t st) {
     a.local_smem = 1;
     smem = base + local_smem(a.m.nx, a.adaptation);
   }
-  auto kern = fine_kernel<T, S, G, NT>;
+  auto kern = fine_kernel<T, S, G, NT, AD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (C > 8) {
@@ -1895,6 +1897,12 @@ static cudaError_t launch_T(FineArgs a, int C, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int T, int S, int G, int NT>
+static cudaError_t launch_T(const FineArgs& a, int C, cudaStream_t st) {
+  return a.adaptation ? launch_TA<T, S, G, NT, true>(a, C, st)
+                      : launch_TA<T, S, G, NT, false>(a, C, st);
 }
 
 template <int T>
@@ -1934,6 +1942,8 @@ cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
     // producer/consumer GS pipeline: 7 consumer warps + 1 producer warp
     case 64: return launch_T<2, 16, 4, 128>(a, C, st);   // G8 per-warp rings, 4 warps
     case 128: return launch_T<4, 14, 8, 128>(a, C, st);  // G8 per-warp rings, 4 warps
+      // (8 warps at <= 128 registers: no spills, but the micro loop loses its
+      // ILP and the step takes 1.6x longer)
     case 256: return launch_T<8, 20, -4, 256>(a, C, st);
     case 512: return launch_T<16, 3, 0, 256>(a, C, st);
     default:
