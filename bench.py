@@ -44,7 +44,10 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons, sampled every 50 ms from before the
+    warm-up to after the timed region; `summary(t0, t1)` keeps the samples whose
+    host timestamps fall inside the timed region (nvidia-smi takes a few hundred
+    ms to start, so starting it at the timed region could miss a short one)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -53,35 +56,42 @@ class ClockSampler:
     def __init__(self, index):
         self.index, self.rows, self.proc = index, [], None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
         return self
 
+    def wait_first(self, timeout=5.0):
+        t_end = time.perf_counter() + timeout
+        while self.proc and not self.rows and time.perf_counter() < t_end:
+            time.sleep(0.01)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc:
+            time.sleep(0.06)  # let the sample covering the region's end arrive
             self.proc.terminate()
             self.proc.wait()
 
-    def summary(self):
-        if not self.rows:
+    def summary(self, t0, t1):
+        rows = [r for t, r in self.rows if t0 <= t <= t1 + 0.06]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6]) if v == "Active"})
+        reasons = sorted({n for r in rows for n, v in zip(names, r[2:6]) if v == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
 
 
 def dist_env():
@@ -216,6 +226,8 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    clk = ClockSampler(dev_index).start()
+    clk.wait_first()
     # warm-up (untimed)
     for _ in range(args.warmup):
         ens.load(rho_d, g_d)
@@ -227,17 +239,20 @@ def main():
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev_index) as clk:
-        barrier()
-        t0.record()
-        for i in range(args.steps):
-            starts[i].record()
-            ens.load(rho_d, g_d)
-            kstart[i].record()
-            ens.run(NSTEPS, check=False)
-            ends[i].record()
-        t1.record()
-        barrier()
+    barrier()
+    h0 = time.perf_counter()
+    t0.record()
+    for i in range(args.steps):
+        starts[i].record()
+        ens.load(rho_d, g_d)
+        kstart[i].record()
+        ens.run(NSTEPS, check=False)
+        ends[i].record()
+    t1.record()
+    barrier()
+    h1 = time.perf_counter()
+    clk.stop()
+    clocks = clk.summary(h0, h1)
     ens.dev.check()
     total_ms = maxr(t0.elapsed_time(t1))
     kern_ms = [kstart[i].elapsed_time(ends[i]) for i in range(args.steps)]
@@ -304,7 +319,7 @@ def main():
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": args.steps,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
             **extra,
         }

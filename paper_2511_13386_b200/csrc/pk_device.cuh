@@ -122,16 +122,15 @@ __device__ void block_pairwise2(F1 x1, F2 x2, const PwPlan& P, double* scratch, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarp = blockDim.x >> 5;
   const int W = P.nleaf + P.nnode;
-  for (int l0 = 4 * warp; l0 < P.nleaf; l0 += 4 * nwarp) {
-    const int l = l0 + (lane >> 3);
-    const bool act = l < P.nleaf;
+  // 2 nleaf leaf tasks (both sums) spread over all 8-lane groups
+  for (int t0 = 4 * warp; t0 < 2 * P.nleaf; t0 += 4 * nwarp) {
+    const int t = t0 + (lane >> 3);
+    const bool act = t < 2 * P.nleaf;
+    const bool second = act && t >= P.nleaf;
+    const int l = second ? t - P.nleaf : t;
     const int off = act ? P.leaf_off[l] : 0, n = act ? P.leaf_len[l] : 0;
-    const double v1 = group_leaf(x1, off, n, act);
-    const double v2 = group_leaf(x2, off, n, act);
-    if (act && (lane & 7) == 0) {
-      scratch[l] = v1;
-      scratch[W + l] = v2;
-    }
+    const double v = group_leaf([&](int i) { return second ? x2(i) : x1(i); }, off, n, act);
+    if (act && (lane & 7) == 0) scratch[second ? W + l : l] = v;
   }
   __syncthreads();
   int start = 0;
