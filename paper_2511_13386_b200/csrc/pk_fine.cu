@@ -323,8 +323,9 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
 }
 
 // J_{i+1/2} = (rho_{i+1}-rho_i)/dx - E*0.5*(rho_i+rho_{i+1})   (fluid.py:48-52)
-__device__ __forceinline__ double flux_J(double r, double rn, double e, double dx) {
-  return (rn - r) / dx - e * 0.5 * (r + rn);
+// ((.)/dx as the correctly rounded Markstein quotient, qdiv in pk_device.cuh)
+__device__ __forceinline__ double flux_J(double r, double rn, double e, double dx, double rdx) {
+  return qdiv(rn - r, dx, rdx) - e * 0.5 * (r + rn);
 }
 
 // Block-wide exclusive scan of per-thread counts; returns the total.
@@ -396,7 +397,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       v.kc[i] = 1;  // adaptation off: all kinetic (hybrid.py:167-168)
       v.ki[i] = 1;
       const double e = v.E[i];
-      const double J = flux_J(v.rho[i], v.rho[in_], e, m.dx);
+      const double J = flux_J(v.rho[i], v.rho[in_], e, m.dx, m.rdx);
       v.J[i] = J;
       v.gJ[i] = J;
       v.dco[i] = (v.fl[in_] - v.fl[ip]) / m.two_dx;
@@ -434,7 +435,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       for (int u = 0; u < U; ++u) {
         const int i = i0 + u * nt;
         if (i < nx) {
-          const double J = flux_J(r0[u], r1[u], e[u], m.dx);
+          const double J = flux_J(r0[u], r1[u], e[u], m.dx, m.rdx);
           J_[i] = J;
           gJ_[i] = J;
         }
@@ -1642,7 +1643,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       }
     } else {
       for (int i = tid; i < nx; i += nt) {
-        v.J[i] = flux_J(v.rho[i], v.rho[wrap(i + 1, nx)], v.E[i], m.dx);
+        v.J[i] = flux_J(v.rho[i], v.rho[wrap(i + 1, nx)], v.E[i], m.dx, m.rdx);
         if (eprev0) v.Eprev[i] = v.E[i];
       }
       __syncthreads();
@@ -1787,7 +1788,7 @@ __global__ void __launch_bounds__(256) lift_kernel(const LiftArgs a) {
   const double* E = a.E + o;
   double *J = a.J + o, *Jc = a.tA + o, *d1 = a.tB + o, *drift = a.tC + o, *R = a.tD + o,
          *Rif = a.tE + o;
-  for (int i = tid; i < nx; i += nt) J[i] = flux_J(rho[i], rho[wrap(i + 1, nx)], E[i], m.dx);
+  for (int i = tid; i < nx; i += nt) J[i] = flux_J(rho[i], rho[wrap(i + 1, nx)], E[i], m.dx, m.rdx);
   __syncthreads();
   const bool higher = a.order >= 2 && a.time_elim == 1;
   if (a.order >= 2) {

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_kernel(const ChainArgs a) {
   for (int i = threadIdx.x; i < nx; i += CHAIN_NT) rho[i] = a.rho_in[(size_t)c * nx + i];
   __syncthreads();
   const double rb = a.rho_bar[c];
-  const double dx = m.dx;
+  const double dx = m.dx, rdx = m.rdx;
   bool have_E = false;
   double mean = 0.0;  // pending zero-mean shift of E (x - 0.0 == x bitwise)
   for (int w = 0; w < a.nwin; ++w) {
@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_kernel(const ChainArgs a) {
           if (i < nx) {
             const int ip = i == 0 ? nx - 1 : i - 1, in_ = i + 1 == nx ? 0 : i + 1;
             const double r = rho[i], rp = rho[ip], rn = rho[in_];
-            const double Ji = (rn - r) / dx - (E[i] - mean) * 0.5 * (r + rn);
-            const double Jp = (r - rp) / dx - (E[ip] - mean) * 0.5 * (rp + r);
+            // (.)/dx as the correctly rounded Markstein quotient (qdiv, pk_device.cuh)
+            const double Ji = qdiv(rn - r, dx, rdx) - (E[i] - mean) * 0.5 * (r + rn);
+            const double Jp = qdiv(r - rp, dx, rdx) - (E[ip] - mean) * 0.5 * (rp + r);
             nr[k] = r + cflu * (Ji - Jp);
           }
         }
