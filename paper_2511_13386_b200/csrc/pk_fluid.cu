@@ -10,18 +10,17 @@
 
 namespace pk {
 
-constexpr int CHAIN_NT = 256;
-constexpr int CHAIN_MAXPER = (MAX_LEAF * 128 + CHAIN_NT - 1) / CHAIN_NT;  // cells per thread
 
 // Field of rho into E, up to the zero-mean shift: returns false on a
 // solvability violation, else E holds cumsum(src - defect/nx) and `mean` its
 // mean, so the field is E[i] - mean (poisson.py:41-54; the subtraction is
 // applied where E is read, with the same rounding).  E doubles as src.
+template <int NT>
 __device__ static bool chain_field(const MeshDev& m, const double* rho, double rb, double* E,
                                    double rtol, int exact_scan, const PwPlan& plan, double* red,
                                    double& mean) {
   const int nx = m.nx;
-  for (int i = threadIdx.x; i < nx; i += CHAIN_NT) E[i] = (rho[i] - rb) * m.dx;
+  for (int i = threadIdx.x; i < nx; i += NT) E[i] = (rho[i] - rb) * m.dx;
   __syncthreads();
   double defect, abssum;
   block_pairwise2([&](int i) { return E[i]; }, [&](int i) { return fabs(rho[i]); }, plan, red,
@@ -29,7 +28,7 @@ __device__ static bool chain_field(const MeshDev& m, const double* rho, double r
   const double scale = abssum * m.dx;
   if (fabs(defect) > rtol * fmax(scale, 2.2250738585072014e-308)) return false;
   const double corr = defect / (double)nx;
-  for (int i = threadIdx.x; i < nx; i += CHAIN_NT) E[i] = E[i] - corr;
+  for (int i = threadIdx.x; i < nx; i += NT) E[i] = E[i] - corr;
   __syncthreads();
   if (exact_scan)
     smem_cumsum(E, E, nx);
@@ -40,9 +39,10 @@ __device__ static bool chain_field(const MeshDev& m, const double* rho, double r
   return true;
 }
 
-// PER: cells per thread (nx <= PER * CHAIN_NT), so the new-rho registers stay unspilled.
-template <int PER>
-__global__ void __launch_bounds__(CHAIN_NT) chain_kernel(const ChainArgs a) {
+// NT threads, PER cells per thread (nx <= PER * NT), so the new-rho registers
+// stay unspilled.
+template <int PER, int NT>
+__global__ void __launch_bounds__(NT) chain_kernel(const ChainArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const MeshDev& m = a.m;
   const int nx = m.nx;
@@ -55,9 +55,9 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_kernel(const ChainArgs a) {
   {
     const int* s = reinterpret_cast<const int*>(m.plan_x);
     int* d = reinterpret_cast<int*>(plan);
-    for (int i = threadIdx.x; i < (int)(sizeof(PwPlan) / 4); i += CHAIN_NT) d[i] = s[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(PwPlan) / 4); i += NT) d[i] = s[i];
   }
-  for (int i = threadIdx.x; i < nx; i += CHAIN_NT) rho[i] = a.rho_in[(size_t)c * nx + i];
+  for (int i = threadIdx.x; i < nx; i += NT) rho[i] = a.rho_in[(size_t)c * nx + i];
   __syncthreads();
   const double rb = a.rho_bar[c];
   const double dx = m.dx, rdx = m.rdx;
@@ -70,10 +70,10 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_kernel(const ChainArgs a) {
     if (nfull > 0 || rem > 0.0) {
       if (w == 0 && a.E_in) {
         // fluid_step: the caller guarantees E matches rho (fluid.py:69-71)
-        for (int i = threadIdx.x; i < nx; i += CHAIN_NT) E[i] = a.E_in[(size_t)c * nx + i];
+        for (int i = threadIdx.x; i < nx; i += NT) E[i] = a.E_in[(size_t)c * nx + i];
         mean = 0.0;
         __syncthreads();
-      } else if (!chain_field(m, rho, rb, E, a.rtol, a.exact_scan, *plan, red, mean)) {
+      } else if (!chain_field<NT>(m, rho, rb, E, a.rtol, a.exact_scan, *plan, red, mean)) {
         // fluid_propagate: the field is refreshed from rho on entry (fluid.py:111-113)
         if (threadIdx.x == 0) set_status(a.status, PK_ERR_SOLVABILITY, c, w);
         return;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_kernel(const ChainArgs a) {
         double nr[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-          const int i = threadIdx.x + k * CHAIN_NT;
+          const int i = threadIdx.x + k * NT;
           if (i < nx) {
             const int ip = i == 0 ? nx - 1 : i - 1, in_ = i + 1 == nx ? 0 : i + 1;
             const double r = rho[i], rp = rho[ip], rn = rho[in_];
@@ -100,27 +100,27 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_kernel(const ChainArgs a) {
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-          const int i = threadIdx.x + k * CHAIN_NT;
+          const int i = threadIdx.x + k * NT;
           if (i < nx) rho[i] = nr[k];
         }
         __syncthreads();
-        if (!chain_field(m, rho, rb, E, a.rtol, a.exact_scan, *plan, red, mean)) {
+        if (!chain_field<NT>(m, rho, rb, E, a.rtol, a.exact_scan, *plan, red, mean)) {
           if (threadIdx.x == 0) set_status(a.status, PK_ERR_SOLVABILITY, c, w);
           return;
         }
       }
     }
     if (a.gout)
-      for (int i = threadIdx.x; i < nx; i += CHAIN_NT) a.gout[cw * nx + i] = rho[i];
+      for (int i = threadIdx.x; i < nx; i += NT) a.gout[cw * nx + i] = rho[i];
     if (a.delta) {
       // new_row[n] = coarse.rho + deltas[n]   (parareal.py:281)
-      for (int i = threadIdx.x; i < nx; i += CHAIN_NT) rho[i] = rho[i] + a.delta[cw * nx + i];
+      for (int i = threadIdx.x; i < nx; i += NT) rho[i] = rho[i] + a.delta[cw * nx + i];
     }
-    for (int i = threadIdx.x; i < nx; i += CHAIN_NT) a.out[cw * nx + i] = rho[i];
+    for (int i = threadIdx.x; i < nx; i += NT) a.out[cw * nx + i] = rho[i];
     __syncthreads();
   }
   if (a.Eout && have_E)
-    for (int i = threadIdx.x; i < nx; i += CHAIN_NT) a.Eout[(size_t)c * nx + i] = E[i] - mean;
+    for (int i = threadIdx.x; i < nx; i += NT) a.Eout[(size_t)c * nx + i] = E[i] - mean;
 }
 
 size_t chain_smem_bytes(int nx) {
@@ -129,20 +129,21 @@ size_t chain_smem_bytes(int nx) {
 
 cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st) {
   const size_t smem = chain_smem_bytes(a.m.nx);
-  const int per = (a.m.nx + CHAIN_NT - 1) / CHAIN_NT;
-  auto go = [&](auto kern) {
+  const int nx = a.m.nx;
+  auto go = [&](auto kern, int nt) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<a.nchain, CHAIN_NT, smem, st>>>(a);
+    kern<<<a.nchain, nt, smem, st>>>(a);
     return cudaGetLastError();
   };
-  if (per <= 2) return go(chain_kernel<2>);
-  if (per <= 4) return go(chain_kernel<4>);
-  if (per <= 8) return go(chain_kernel<8>);
-  if (per <= 16) return go(chain_kernel<16>);
-  if (per <= 32) return go(chain_kernel<32>);
-  return go(chain_kernel<CHAIN_MAXPER>);
+  // more threads for the element passes at large nx (the scan stays on one)
+  if (nx <= 512) return go(chain_kernel<2, 256>, 256);
+  if (nx <= 1024) return go(chain_kernel<4, 256>, 256);
+  if (nx <= 2048) return go(chain_kernel<4, 512>, 512);
+  if (nx <= 4096) return go(chain_kernel<8, 512>, 512);
+  if (nx <= 8192) return go(chain_kernel<16, 512>, 512);
+  return go(chain_kernel<(MAX_LEAF * 128 + 511) / 512, 512>, 512);
 }
 
 // Delta = F - G (parareal.py:429) and the finiteness check of parareal.py:267-269.
