@@ -410,3 +410,30 @@ def test_cfg3_window2_guard_and_relaxed(gold):
     assert eq(out.macro.rho, d["r_rho"]) and eq(out.macro.E, d["r_E"])
     assert eq(out.E_prev, d["r_Eprev"])
     assert digest(out.micro.g.reshape(m.nx, m.nv)) == str(d["r_g_digest"])
+
+
+def test_cfg4_size_hybrid_vs_oracle():
+    """BASELINE cfg4's full grid (8192 x 256, v* = 10, eps(x) bump, thresholds
+    1e-3) from a lifted window restart, 12 hybrid steps: the nv = 256
+    producer/consumer micro phase on listed rows, the global-memory slice phase
+    (listed flips/zeroing, TMA-staged scan) -- bitwise vs the oracle."""
+    c = configs.cfg4()
+    m = c.mesh
+    og = O.make_grid(8192, 256, v_star=10.0)
+    eps = O.EpsProfile.from_function(configs.eps_bump, og)
+    E0 = pk.solve_field(c.rho, c.rho_bar, m, rtol=1e-5)
+    g1 = pk.lift(c.rho, E0, c.eps, m, order=2, time_elim="leading", rho_bar=c.rho_bar)
+    dt = O.stable_dt(og, eps, e_max=float(np.max(np.abs(E0))))
+    p = pk.KineticStepParams(eps=c.eps, dt=dt)
+    th = pk.Thresholds(1e-3, 1e-3)
+    st = pk.HybridState.initial(pk.MacroState(c.rho, E0, 0.0), g1, m)
+    out = pk.hybrid_propagate(st, 12 * dt, p, th, pk.HybridOptions(), m, c.rho_bar,
+                              field_rtol=1e-5)
+    ost = O.HState.start(c.rho, O.field(c.rho, c.rho_bar, og, 1e-5),
+                         O.lift(c.rho, O.field(c.rho, c.rho_bar, og, 1e-5), eps, og, order=2,
+                                time_elim="leading", rho_bar=c.rho_bar), 0.0)
+    ref = O.hpropagate(ost, 12 * dt, dt, eps, 1e-3, 1e-3, O.HOpts(), og, c.rho_bar, 1e-5)
+    assert 0.0 < ref.kc.mean() < 1.0  # mixed kinetic / fluid
+    assert eq(out.labels.kinetic_cells, ref.kc) and eq(out.labels.kinetic_ifaces, ref.ki)
+    assert eq(out.macro.rho, ref.rho) and eq(out.macro.E, ref.E) and eq(out.E_prev, ref.E_prev)
+    assert eq(out.micro.g.reshape(m.nx, m.nv), ref.g)
