@@ -1871,10 +1871,22 @@ static size_t local_smem(int nx, int adaptation) {
 template <int T, int S, int G, int NT, bool AD>
 static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   const size_t base = base_smem(a.m.nv, T, S, G, NT);
-  // slice vectors on chip when two CTAs still fit per SM
+  // slice vectors on chip when they fit: two CTAs per SM when the grid needs
+  // them, the whole SM's shared memory when the grid has one CTA per SM
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t need = base + local_smem(a.m.nx, a.adaptation);
+  // half the cluster if that puts the slice vectors on chip (one CTA per SM)
+  if (need > 112 * 1024 && need <= 226 * 1024 && C >= 2 && (size_t)a.B * (C / 2) <= (size_t)num_sms)
+    C /= 2;
+  const size_t limit = (size_t)a.B * C <= (size_t)num_sms ? 226 * 1024 : 112 * 1024;
   size_t smem = base + STAGE_NS * STAGE_CH * 8;  // scan staging ring
   a.local_smem = 0;
-  if (base + local_smem(a.m.nx, a.adaptation) <= 112 * 1024) {
+  if (base + local_smem(a.m.nx, a.adaptation) <= limit) {
     a.local_smem = 1;
     smem = base + local_smem(a.m.nx, a.adaptation);
   }

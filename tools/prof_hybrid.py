@@ -76,7 +76,7 @@ def main():
               % tuple(int(x) // ns for x in cc[:5]))
         print("   field cycles/step: src %d, pairwise2 %d, corr %d, cumsum %d, mean %d, sub %d"
               % tuple(int(x) // ns for x in cc[8:14]))
-        print("   prologue cycles: %d" % int(cc[6]))
+        print("   prologue cycles: %d, slice vectors in shared memory: %s" % (int(cc[6]), bool(cc[15])))
         print("   prepare cycles/step: J %d, R+labels %d, flips %d, lift %d, bm %d, dco+zlist %d, "
               "zero %d, klist %d, kstream %d" % tuple(int(x) // ns for x in cc[16:25]))
         print("   rows/step: flipped %.1f, zeroed %.1f, kinetic %.1f"
