@@ -287,8 +287,11 @@ def main():
     d2h = (rho_o.numel() * 2 + g_o.numel()) * 8 * ws
 
     extra = {}
-    if rank == 0 and not args.no_parareal:
-        extra["parareal"] = parareal_cfg2()
+    if not args.no_parareal:
+        # collective: every rank runs the engine (windows dealt across ranks)
+        par = parareal_cfg2(barrier, maxr)
+        if rank == 0:
+            extra["parareal"] = par
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "fine_kernel_traffic.json")
     if os.path.exists(tpath):
@@ -328,8 +331,11 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def parareal_cfg2():
-    """BASELINE configs[1] wall time on this GPU through the drop-in run()."""
+def parareal_cfg2(barrier, maxr):
+    """BASELINE configs[1] through the drop-in run() on every rank (the engine
+    deals the windows of each iteration across ranks and all-gathers the fine
+    results).  Wall time = CUDA-event span on each rank's device timeline
+    (host gaps between launches included), max over ranks."""
     import torch
 
     import paper_2511_13386_b200 as pk
@@ -339,10 +345,13 @@ def parareal_cfg2():
     cfg = pk.PararealConfig(eps=1e-2, t_final=0.5, ng=16, k_max=5, tol=1e-10,
                             options=pk.HybridOptions(adaptation=False))
     pk.run(cfg, c.rho, c.g, c.mesh, c.rho_bar)  # warm-up
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     res = pk.run(cfg, c.rho, c.g, c.mesh, c.rho_bar)
-    wall = time.perf_counter() - t0
+    e1.record()
+    barrier()
+    wall = maxr(e0.elapsed_time(e1) * 1e-3)
     tm = res.ledger.timings
     E0 = pk.solve_field(c.rho, c.rho_bar, c.mesh)
     _, kin_p = pk.parareal.default_params(cfg, c.mesh, E0)
@@ -351,8 +360,8 @@ def parareal_cfg2():
     fine_updates = sum(16 - k for k in range(res.iterations)) * per_window
     return {"config": "cfg2: Nx=256, Nv=64, eps=1e-2, T=0.5, 16 slices, reference dt",
             "wall_s": wall, "iterations": res.iterations, "status": res.status,
-            "fine_s": tm.fine_total, "correction_s": tm.correction_total,
-            "coarse_sweep_s": tm.coarse_sweep,
+            "fine_s": maxr(tm.fine_total), "correction_s": maxr(tm.correction_total),
+            "coarse_sweep_s": maxr(tm.coarse_sweep),
             "fine_cell_updates": fine_updates,
             "fine_cell_updates_per_s": fine_updates / max(tm.fine_total, 1e-12),
             "reference_cpu_s_build_container_1core": 41.7}
