@@ -67,6 +67,8 @@ typedef struct pk_phase {
   const double* kappa2;  /* [B*nx]  eps_i * -expm1(-dt/eps_i**2) */
   const double* cmac;    /* [B*nx]  dt / (eps_i * dx)               kinetic.py:240 */
   const double* cmac_scalar; /* [B] cmac when uniform in x (constant eps), else NaN */
+  const double* kappa1_scalar; /* [B] kappa1 when uniform in x, else NaN (or NULL) */
+  const double* kappa2_scalar; /* [B] kappa2 when uniform in x, else NaN (or NULL) */
 } pk_phase;
 
 /* Hybrid options (hybrid.py:45-55) and thresholds (adaptation.py:80-90). */

@@ -36,6 +36,8 @@ class PkPhase(C.Structure):
         ("nsteps", C.c_void_p), ("dt", C.c_void_p), ("cflu", C.c_void_p),
         ("kappa1", C.c_void_p), ("kappa2", C.c_void_p), ("cmac", C.c_void_p),
         ("cmac_scalar", C.c_void_p),
+        ("kappa1_scalar", C.c_void_p),
+        ("kappa2_scalar", C.c_void_p),
     ]
 
 

@@ -297,6 +297,8 @@ int32_t pk_fine_propagate(pk_ctx* c, int32_t B, double* rho, double* E, double* 
     a.ph[p].k2 = phases[p].kappa2;
     a.ph[p].cmac = phases[p].cmac;
     a.ph[p].cmacs = phases[p].cmac_scalar;
+    a.ph[p].k1s = phases[p].kappa1_scalar;
+    a.ph[p].k2s = phases[p].kappa2_scalar;
     if (!a.ph[p].nsteps || !a.ph[p].dt || !a.ph[p].cflu || !a.ph[p].k1 || !a.ph[p].k2 ||
         !a.ph[p].cmac)
       return fail(c, PK_ERR_BAD_ARG, "pk_fine_propagate: incomplete phase");

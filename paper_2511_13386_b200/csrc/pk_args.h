@@ -31,6 +31,8 @@ struct PhaseDev {
   const double* k2;     // [B*nx] eps_i * -expm1(-dt/eps_i^2)
   const double* cmac;   // [B*nx] dt / (eps_i * dx)         (kinetic.py:240)
   const double* cmacs;  // [B] the common value when uniform in x, else NaN
+  const double* k1s;    // [B] likewise for k1 (or null)
+  const double* k2s;    // [B] likewise for k2 (or null)
 };
 
 struct FineArgs {

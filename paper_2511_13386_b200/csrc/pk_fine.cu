@@ -958,6 +958,9 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   const uint32_t s_vx = smem_u32(sm.vx), s_M = smem_u32(sm.M), s_xiM = smem_u32(sm.xiM);
   const uint32_t s_ring = smem_u32(ring), s_mbar = smem_u32(mbar);
   const double dx = m.dx, rdx = m.rdx, dv3 = m.dv3;
+  const double NaN_ = __longlong_as_double(0x7ff8000000000000LL);
+  const double k1u = P.k1s ? P.k1s[v.b] : NaN_, k2u = P.k2s ? P.k2s[v.b] : NaN_;
+  const bool kuni = k1u == k1u && k2u == k2u;
   auto rowid = [&](int p) { return DENSE ? p : __ldcg(v.klist + p); };
 
   if (lane == 0) fence_proxy_async_global();  // rows written by the generic proxy, read by TMA
@@ -1058,8 +1061,10 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
         c_vco = sg > 0 ? vco : (sg < 0 ? -vco : 0.0);
         c_dco = __ldcg(v.dco + r);
         c_J = __ldcg(v.gJ + r);
-        c_k1 = __ldg(P.k1 + o + r);
-        c_k2 = __ldg(P.k2 + o + r);
+        if (!kuni) {  // constant eps: kappa1/2 are per-slice scalars
+          c_k1 = __ldg(P.k1 + o + r);
+          c_k2 = __ldg(P.k2 + o + r);
+        }
         // neighbour direction rides in the sign bit of the row id
         c_row = sg > 0 ? r : -1 - r;
       }
@@ -1105,8 +1110,8 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
     const double svco = __shfl_sync(FULL, c_vco, src);
     const double dc = __shfl_sync(FULL, c_dco, src);
     const double J = __shfl_sync(FULL, c_J, src);
-    const double k1 = __shfl_sync(FULL, c_k1, src);
-    const double k2 = __shfl_sync(FULL, c_k2, src);
+    const double k1 = kuni ? k1u : __shfl_sync(FULL, c_k1, src);
+    const double k2 = kuni ? k2u : __shfl_sync(FULL, c_k2, src);
     const bool up = rsg >= 0;          // E > 0 (or 0): velocity neighbour j-1
     const int i = up ? rsg : -1 - rsg;
     double bx = 0.0, bsq = 0.0;

@@ -54,6 +54,8 @@ class Phase:
     k2: np.ndarray       # [B, nx]
     cmac: np.ndarray     # [B, nx]
     cmac_scalar: np.ndarray = None  # [B]: the common cmac when uniform in x, else NaN
+    k1_scalar: np.ndarray = None    # [B]: the common kappa1 when uniform in x, else NaN
+    k2_scalar: np.ndarray = None    # [B]: the common kappa2 when uniform in x, else NaN
 
 
 def eps_rows(eps, nx: int) -> np.ndarray:
@@ -100,8 +102,11 @@ def make_phase(mesh: PhaseMesh, eps_list, dt_list, nsteps_list) -> Phase:
         k2[b] = per_value(e, lambda v: relaxation_coefficients(dt, v)[1])
         cm[b] = per_value(e, lambda v: dt / (v * dx))
         cflu[b] = m2 * (dt / dx)
-    cs = np.array([row[0] if (row == row[0]).all() else np.nan for row in cm])
-    return Phase(np.asarray(nsteps_list, dtype=np.int32), dts, cflu, k1, k2, cm, cs)
+    def uniform(a):  # per slice: the common value of a row, else NaN
+        return np.array([row[0] if (row == row[0]).all() else np.nan for row in a])
+
+    return Phase(np.asarray(nsteps_list, dtype=np.int32), dts, cflu, k1, k2, cm, uniform(cm),
+                 uniform(k1), uniform(k2))
 
 
 @dataclass
@@ -225,11 +230,13 @@ class Device:
         torch = _torch()
         dev = dict(
             nsteps=self.t(ph.nsteps.astype(np.int32)), dt=self.t(ph.dt), cflu=self.t(ph.cflu),
-            k1=self.t(ph.k1), k2=self.t(ph.k2), cmac=self.t(ph.cmac), cs=self.t(ph.cmac_scalar))
+            k1=self.t(ph.k1), k2=self.t(ph.k2), cmac=self.t(ph.cmac), cs=self.t(ph.cmac_scalar),
+            k1s=self.t(ph.k1_scalar), k2s=self.t(ph.k2_scalar))
         s = _native.PkPhase()
         s.nsteps, s.dt, s.cflu = _ptr(dev["nsteps"]), _ptr(dev["dt"]), _ptr(dev["cflu"])
         s.kappa1, s.kappa2, s.cmac = _ptr(dev["k1"]), _ptr(dev["k2"]), _ptr(dev["cmac"])
         s.cmac_scalar = _ptr(dev["cs"])
+        s.kappa1_scalar, s.kappa2_scalar = _ptr(dev["k1s"]), _ptr(dev["k2s"])
         del torch
         return s, dev
 
