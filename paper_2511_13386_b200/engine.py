@@ -250,7 +250,10 @@ class Device:
         ph_structs, hyb, keep = prepared
         gb = self.scratch("gb", (B, nx, nv))
         self.reserve(B)
-        flags = self.t(np.asarray(init_flags, dtype=np.uint8))
+        # a device tensor is used as is (no per-call upload: a pageable copy
+        # would block the host until the stream drains)
+        flags = (init_flags if isinstance(init_flags, _torch().Tensor)
+                 else self.t(np.asarray(init_flags, dtype=np.uint8)))
         rc = self.lib.pk_fine_propagate(
             self.ctx, B, _ptr(rho), _ptr(E), _ptr(Eprev), _ptr(kc), _ptr(ki), _ptr(g), _ptr(gb),
             _ptr(rho_bar), _ptr(flags), ph_structs, C.byref(hyb), float(rtol),
