@@ -14,6 +14,11 @@ time (BASELINE configs[1]) on this GPU.
 
 from __future__ import annotations
 
+import os
+
+# before any CUDA context exists (see paper_2511_13386_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import argparse
 import json
 import os

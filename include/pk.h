@@ -95,6 +95,9 @@ void pk_destroy(pk_ctx* ctx);
 const char* pk_last_error(const pk_ctx* ctx);
 int32_t pk_reserve(pk_ctx* ctx, int32_t max_slices);              /* grow scratch */
 int32_t pk_status_read(pk_ctx* ctx, pk_status* out, int32_t clear); /* synchronises */
+/* Same record, ordered on `stream` only (waits for the work queued on that
+   stream, not for the whole device): for contexts driven from several streams. */
+int32_t pk_status_read_stream(pk_ctx* ctx, pk_status* out, int32_t clear, void* stream);
 int32_t pk_version(void);
 /* diagnostics: accumulate per-phase clock64 counters of slice 0 into a device
  * array of 6 int64 [micro, barrier, slice finish, slice prepare, barrier,

@@ -64,6 +64,7 @@ SIGNATURES = {
     "pk_last_error": (C.c_char_p, [C.c_void_p]),
     "pk_reserve": (C.c_int32, [C.c_void_p, C.c_int32]),
     "pk_status_read": (C.c_int32, [C.c_void_p, C.POINTER(PkStatus), C.c_int32]),
+    "pk_status_read_stream": (C.c_int32, [C.c_void_p, C.POINTER(PkStatus), C.c_int32, C.c_void_p]),
     "pk_fine_propagate": (C.c_int32, [
         C.c_void_p, C.c_int32,
         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -247,6 +247,22 @@ int32_t pk_reserve(pk_ctx* c, int32_t max_slices) {
   return ensure(c, max_slices);
 }
 
+int32_t pk_status_read_stream(pk_ctx* c, pk_status* out, int32_t clear, void* stream) {
+  if (!c || !out) return PK_ERR_BAD_ARG;
+  cudaSetDevice(c->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  pk::Status s;
+  cudaError_t e = cudaMemcpyAsync(&s, c->d_status, sizeof(s), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "status copy");
+  out->code = s.code;
+  out->slice = s.slice;
+  out->step = s.step;
+  out->pad = 0;
+  if (clear) cudaMemsetAsync(c->d_status, 0, sizeof(pk::Status), st);
+  return PK_OK;
+}
+
 int32_t pk_status_read(pk_ctx* c, pk_status* out, int32_t clear) {
   if (!c || !out) return PK_ERR_BAD_ARG;
   cudaSetDevice(c->device);

@@ -215,6 +215,15 @@ class Device:
             msg = self.lib.pk_last_error(self.ctx)
             raise_for(code, f"{what}: {msg.decode() if msg else ''}")
 
+    def check_stream(self, stream):
+        """Raise this context's latched status after the work queued on
+        `stream` (a torch.cuda.Stream) -- without synchronising the device."""
+        st = _native.PkStatus()
+        self._rc(self.lib.pk_status_read_stream(self.ctx, C.byref(st), 1,
+                                                C.c_void_p(stream.cuda_stream)), "status")
+        if st.code:
+            raise_for(st.code, f"slice {st.slice}, step {st.step}")
+
     def check(self):
         """Synchronise and raise the latched device status, if any."""
         st = _native.PkStatus()
@@ -295,20 +304,35 @@ class Device:
               exact_scan=True, E_in=None, m2=None):
         """Coarse chains: rho_in [nchain, nx], out/gout/delta [nchain, nwin, nx]."""
         nchain, nwin = out.shape[0], out.shape[1]
-        dx = self.mesh.dx
-        m2 = self.mesh.vgrid.m2 if m2 is None else m2
         nfull = np.asarray(nfull, dtype=np.int32).reshape(nchain, nwin)
         rem = np.asarray(rem, dtype=float).reshape(nchain, nwin)
-        cf = np.full((nchain, nwin), m2 * (dt_full / dx))
+        sched = self.chain_schedule(nfull, rem, dt_full, m2)
+        self.chain_raw(rho_in, out, gout, E_out, delta, sched, dt_full, rho_bar, rtol, exact_scan,
+                       E_in)
+        self._keepalive = sched
+
+    def chain_schedule(self, nfull, rem, dt_full, m2=None):
+        """Device copies of a chain's per-window step schedule (nfull, rem and
+        the cflu factors m2 dt/dx), reusable across chain_raw calls."""
+        m2 = self.mesh.vgrid.m2 if m2 is None else m2
+        dx = self.mesh.dx
+        nfull = np.atleast_2d(np.asarray(nfull, dtype=np.int32))
+        rem = np.atleast_2d(np.asarray(rem, dtype=float))
+        cf = np.full(nfull.shape, m2 * (dt_full / dx))
         cr = np.vectorize(lambda r: m2 * (r / dx) if r > 0.0 else 0.0)(rem) if rem.size else rem
-        d_nf, d_rem, d_cf, d_cr = self.t(nfull), self.t(rem), self.t(cf), self.t(np.asarray(cr, float))
+        return (self.t(nfull), self.t(rem), self.t(cf), self.t(np.asarray(cr, float)))
+
+    def chain_raw(self, rho_in, out, gout, E_out, delta, sched, dt_full, rho_bar, rtol,
+                  exact_scan=True, E_in=None):
+        """pk_coarse_chain on the current stream with a prepared schedule (no uploads)."""
+        nchain, nwin = out.shape[0], out.shape[1]
+        d_nf, d_rem, d_cf, d_cr = sched
         rc = self.lib.pk_coarse_chain(
             self.ctx, nchain, nwin, _ptr(rho_in), _ptr(E_in), _ptr(out), _ptr(gout), _ptr(E_out),
             _ptr(delta),
             _ptr(d_nf), _ptr(d_rem), _ptr(d_cf), _ptr(d_cr), float(dt_full), _ptr(rho_bar),
             float(rtol), int(bool(exact_scan)), self.stream)
         self._rc(rc, "pk_coarse_chain")
-        self._keepalive = (d_nf, d_rem, d_cf, d_cr)
 
     def field(self, rho, rho_bar, E, rtol, exact_scan=True):
         self.reserve(rho.shape[0])

@@ -296,6 +296,13 @@ class _Engine:
         self.be = backend(self) if backend is not None else DeviceBackend(self)
         self.row = self.be.tensor(np.repeat(np.asarray(rho0, float)[None], ng + 1, 0))
         self.G = torch.empty_like(self.row)
+        self.overlap = None
+
+    def close(self):
+        """Wait for any speculative work still in flight (buffers stay owned
+        until it has finished)."""
+        if self.overlap is not None:
+            self.overlap.sync()
 
     def coarse_sweep(self):
         """Row 0 (parareal.py:210-229); default field guard as the reference."""
@@ -317,6 +324,10 @@ class _Engine:
         if B == 0:
             # every window converged by prefix exactness: row_{k+1} == row_k
             return 0.0, self.row[:0], np.zeros(ng + 1), targets, 0.0, 0.0
+        if self.comm.size == 1 and isinstance(be, DeviceBackend) and OVERLAP:
+            if self.overlap is None:
+                self.overlap = _Overlap.get(self)
+            return self.overlap.iterate(k)
         t0 = be.clock()
         size, rank = self.comm.size, self.comm.rank
         if size == 1:
@@ -355,6 +366,203 @@ class _Engine:
             fracs[n] = float(kc_h[j]) / nx
         self.row, self.G = new, Gn
         return err, delta, fracs, targets, be.seconds(t0, t1), be.seconds(t2, t3)
+
+
+# Overlap the coarse correction with the next iteration's fine windows on a
+# single GPU (tests can switch it off to compare the two schedules).
+OVERLAP = True
+TIMELINE = False    # diagnostics: record per-window event times (tools/par_timing.py)
+_DEVICE_POOLS: dict = {}
+
+
+def _device_pool(mesh, device, ng):
+    """Two solver contexts per window (one per iteration parity) plus one for
+    the correction, cached per (mesh, device, ng)."""
+    key = (id(mesh), str(device), ng)
+    pool = _DEVICE_POOLS.get(key)
+    if pool is None or pool[0] is not mesh:
+        devs = [None] + [[Device(mesh, device), Device(mesh, device)] for _ in range(ng)]
+        pool = _DEVICE_POOLS[key] = (mesh, devs, Device(mesh, device))
+    return pool[1], pool[2]
+
+
+class _Overlap:
+    """Single-GPU parareal schedule with the coarse correction overlapped with
+    the fine windows of the next iteration.
+
+    F for window n of iteration k+1 needs only row_{k+1}[n-1], which the
+    correction of iteration k produces window by window.  So each window's F
+    is enqueued, speculatively, behind the correction step that produces its
+    input -- on the window's own stream and solver context (two per window,
+    one per iteration parity, so workspaces and status records never mix) --
+    and its jump behind the step that produces G(row_{k+1}[n-1]).  The
+    correction runs window by window on its own stream.  Events order all of
+    it; the host reads err (correction stream only) and the statuses of the
+    work it consumed.  Every value is the same function of the same inputs as
+    in the phase-by-phase schedule, so ledgers are bitwise identical; the
+    speculative work of an iteration that never happens is dropped unread."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, eng):
+        """Resources are cached per (mesh, device, schedule, parameters): a
+        repeated run reuses the prepared phases, buffers and streams."""
+        cfg = eng.cfg
+        key = (id(eng.mesh), str(eng.be.device), cfg.ng, id(cfg.eps), eng.kin_p.dt,
+               eng.fluid_p.dt, eng.fluid_p.m2, eng.rtol_f, repr(eng.knobs), tuple(eng.sf),
+               tuple(eng.sc))
+        ov = cls._cache.get(key)
+        if ov is None or ov.mesh is not eng.mesh or ov.eps is not cfg.eps:
+            ov = cls._cache[key] = cls(eng)
+        ov.sync()
+        ov.eng = eng
+        ov.Rn = eng.torch.empty_like(eng.row)
+        ov.Gn = eng.torch.empty_like(eng.G)
+        return ov
+
+    def __init__(self, eng):
+        torch = eng.torch
+        self.torch, self.eng = torch, eng
+        self.mesh, self.eps = eng.mesh, eng.cfg.eps  # keep the key objects alive
+        cfg, mesh, be = eng.cfg, eng.mesh, eng.be
+        ng, nx, nv = cfg.ng, eng.nx, eng.nv
+        dv = be.device
+        self.devs, self.cdev = _device_pool(mesh, dv, ng)
+        self.fs = [None] + [[torch.cuda.Stream(dv), torch.cuda.Stream(dv)] for _ in range(ng)]
+        self.cs = torch.cuda.Stream(dv)
+        f64 = dict(dtype=torch.float64, device=dv)
+        self.D = torch.zeros((2, ng + 1, nx), **f64)           # jumps per parity
+        self.K = torch.zeros((2, ng + 1), dtype=torch.int64, device=dv)
+        self.Rn = torch.empty_like(eng.row)                     # next rows
+        self.Gn = torch.empty_like(eng.G)                       # next G cache
+        self.buf = [None] + [[dict(rho=torch.empty((1, nx), **f64), E=torch.empty((1, nx), **f64),
+                                   Ep=torch.empty((1, nx), **f64),
+                                   kc=torch.ones((1, nx), dtype=torch.uint8, device=dv),
+                                   ki=torch.ones((1, nx), dtype=torch.uint8, device=dv),
+                                   g=torch.empty((1, nx, nv), **f64)) for _ in range(2)]
+                             for _ in range(ng)]
+        eps, dt = cfg.eps, eng.kin_p.dt
+        self.prep = [None] * (ng + 1)
+        self.flags = [None] * (ng + 1)
+        self.sched = [None] * (ng + 1)
+        phases = {}
+        for n in range(1, ng + 1):
+            nf, rem = eng.sf[n - 1]
+            key = (nf, rem)
+            if key not in phases:
+                phases[key] = [make_phase(mesh, [eps], [dt], [nf]),
+                               make_phase(mesh, [eps], [rem if rem > 0.0 else dt],
+                                          [1 if rem > 0.0 else 0])]
+            self.prep[n] = [self.devs[n][q].prepare_fine(1, phases[key], eng.knobs, [eps])
+                            for q in range(2)]
+            # window 1 starts from the true g0, the others from a lift (parareal.py:169-178)
+            self.flags[n] = be.dev.t(np.array([2 if n == 1 else 3], dtype=np.uint8))
+            self.sched[n] = self.cdev.chain_schedule([eng.sc[n - 1][0]], [eng.sc[n - 1][1]],
+                                                     eng.fluid_p.dt, eng.fluid_p.m2)
+        self.ev_row = [torch.cuda.Event(enable_timing=TIMELINE) for _ in range(ng + 1)]
+        self.ev_fstart = [[torch.cuda.Event(enable_timing=True) for _ in range(ng + 1)]
+                          for _ in range(2)]
+        self.ev_jump = [[torch.cuda.Event(enable_timing=True) for _ in range(ng + 1)]
+                        for _ in range(2)]
+        self.spec = None    # the iteration whose fine windows are already enqueued
+
+    def _fine(self, q, n, x_row, wait):
+        """Enqueue F for window n (parity q) from x_row [nx] after `wait`."""
+        torch, eng = self.torch, self.eng
+        s, dev, b = self.fs[n][q], self.devs[n][q], self.buf[n][q]
+        with torch.cuda.stream(s):
+            if wait is not None:
+                s.wait_event(wait)
+            if TIMELINE:
+                self.ev_fstart[q][n].record(s)
+            b["rho"][0].copy_(x_row)
+            if n == 1:
+                b["g"][0].copy_(eng.be.g0)
+            b["kc"].fill_(1)
+            b["ki"].fill_(1)
+            dev.fine(b["rho"], b["E"], b["Ep"], b["kc"], b["ki"], b["g"], eng.be.rb1,
+                     self.flags[n], None, eng.knobs, [eng.cfg.eps], eng.rtol_f,
+                     prepared=self.prep[n][q])
+            self.K[q, n] = b["kc"].sum(dtype=torch.int64)
+
+    def _jump(self, q, n, G_row, wait):
+        """Enqueue Delta = F - G for window n (parity q) after `wait`."""
+        torch = self.torch
+        s = self.fs[n][q]
+        with torch.cuda.stream(s):
+            if wait is not None:
+                s.wait_event(wait)
+            self.devs[n][q].jump(self.buf[n][q]["rho"][0], G_row, self.D[q, n])
+            self.ev_jump[q][n].record(s)
+
+    def iterate(self, k):
+        torch, eng = self.torch, self.eng
+        cfg, ng, nx = eng.cfg, eng.cfg.ng, eng.nx
+        q = k & 1
+        self._t_iter = time.perf_counter()
+        targets = list(range(k + 1, ng + 1))
+        R, Gc, Rn, Gn = eng.row, eng.G, self.Rn, self.Gn
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(torch.cuda.current_stream())
+        if self.spec != k:   # nothing speculative for this iteration: launch its windows now
+            for n in targets:
+                self._fine(q, n, R[n - 1], start)
+                self._jump(q, n, Gc[n], None)
+        speculate = k + 1 < cfg.k_max and k + 2 <= ng
+        cs, cdev = self.cs, self.cdev
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(cs):
+            cs.wait_event(start)
+            Rn.copy_(R)           # prefix rows 0..k are final (prefix exactness)
+            Gn.copy_(Gc)
+            c0.record(cs)
+        for n in targets:
+            with torch.cuda.stream(cs):
+                cs.wait_event(self.ev_jump[q][n])
+                # row_{k+1}[n] = G(row_{k+1}[n-1]) + Delta_k[n]; gout = G(row_{k+1}[n-1])
+                cdev.chain_raw(Rn[n - 1].view(1, nx), Rn[n].view(1, 1, nx), Gn[n].view(1, 1, nx),
+                               None, self.D[q, n].view(1, 1, nx), self.sched[n], eng.fluid_p.dt,
+                               eng.be.rb1, SOLVABILITY_RTOL if eng.rtol is None else eng.rtol)
+                self.ev_row[n].record(cs)
+            if speculate:
+                if n + 1 <= ng:
+                    self._fine(q ^ 1, n + 1, Rn[n], self.ev_row[n])
+                if n >= k + 2:
+                    self._jump(q ^ 1, n, Gn[n], self.ev_row[n])
+        with torch.cuda.stream(cs):
+            c1.record(cs)
+            cdev.maxdiff(Rn, R, eng.be.err_d)
+            self.host_enqueue_s = time.perf_counter() - self._t_iter
+            err = float(eng.be.err_d.item())     # waits for the correction stream only
+        self.spec = k + 1 if speculate else None
+        cdev.check_stream(cs)
+        for n in targets:
+            self.devs[n][q].check_stream(self.fs[n][q])
+        delta = self.D[q, k + 1:].clone()
+        kc = self.K[q].cpu().numpy()
+        fracs = np.zeros(ng + 1)
+        for n in targets:
+            fracs[n] = float(kc[n]) / nx
+        # fine span seen from this iteration's start (speculative windows may
+        # have finished during the previous correction: then ~0)
+        t_fine = max(0.0, max(start.elapsed_time(self.ev_jump[q][n]) for n in targets) * 1e-3)
+        t_corr = c0.elapsed_time(c1) * 1e-3
+        if TIMELINE:
+            self.timeline = [(n, start.elapsed_time(self.ev_fstart[q][n]),
+                              start.elapsed_time(self.ev_jump[q][n]),
+                              start.elapsed_time(self.ev_row[n])) for n in targets]
+        # swap the row / G buffers: the speculative windows read the new ones
+        eng.row, self.Rn = Rn, R
+        eng.G, self.Gn = Gn, Gc
+        return err, delta, fracs, targets, t_fine, t_corr
+
+    def sync(self):
+        for pair in self.fs[1:]:
+            for s in pair:
+                s.synchronize()
+        self.cs.synchronize()
+        self.spec = None
 
 
 _ENGINES: dict = {}
@@ -511,7 +719,9 @@ def run(cfg: PararealConfig, rho0, g0, mesh: PhaseMesh, rho_bar: float) -> RunRe
                 status = "converged"
                 break
     finally:
-        _ENGINES.pop(id(ledger), None)
+        eng = _ENGINES.pop(id(ledger), None)
+        if eng is not None:
+            eng.close()
     ledger.timings.wall_total = time.perf_counter() - wall_tic
     return RunResult(status=status, iterations=len(ledger.err), ledger=ledger,
                      boundary_rho=ledger.rho[-1], kinetic_fraction=ledger.kinetic_fraction,
