@@ -128,7 +128,10 @@ size_t chain_smem_bytes(int nx) {
 }
 
 cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st) {
-  const size_t smem = chain_smem_bytes(a.m.nx);
+  // The chain is one latency-bound CTA per chain: claim (nearly) a whole SM's
+  // shared memory so that no fine-propagator CTA is co-scheduled beside it
+  // when the correction overlaps the fine windows (parareal._Overlap).
+  const size_t smem = chain_smem_bytes(a.m.nx) > 200 * 1024 ? chain_smem_bytes(a.m.nx) : 200 * 1024;
   const int nx = a.m.nx;
   auto go = [&](auto kern, int nt) {
     cudaError_t e =

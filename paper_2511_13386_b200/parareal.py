@@ -429,8 +429,16 @@ class _Overlap:
         ng, nx, nv = cfg.ng, eng.nx, eng.nv
         dv = be.device
         self.devs, self.cdev = _device_pool(mesh, dv, ng)
-        self.fs = [None] + [[torch.cuda.Stream(dv), torch.cuda.Stream(dv)] for _ in range(ng)]
-        self.cs = torch.cuda.Stream(dv)
+        # torch hands out streams from a pool of 32 per priority: the
+        # correction (the critical path) takes a high-priority stream of its
+        # own; each window one low-priority stream for both parities (windows
+        # beyond 32 share streams, which only serialises them)
+        self.cs = torch.cuda.Stream(dv, priority=-1)
+        # status reads wait on one window's jump event only, not on the
+        # speculative work queued behind it on the window's stream
+        self.ss = torch.cuda.Stream(dv, priority=-1)
+        ws = [torch.cuda.Stream(dv) for _ in range(ng)]
+        self.fs = [None] + [[s, s] for s in ws]
         f64 = dict(dtype=torch.float64, device=dv)
         self.D = torch.zeros((2, ng + 1, nx), **f64)           # jumps per parity
         self.K = torch.zeros((2, ng + 1), dtype=torch.int64, device=dv)
@@ -538,7 +546,8 @@ class _Overlap:
         self.spec = k + 1 if speculate else None
         cdev.check_stream(cs)
         for n in targets:
-            self.devs[n][q].check_stream(self.fs[n][q])
+            self.ss.wait_event(self.ev_jump[q][n])
+            self.devs[n][q].check_stream(self.ss)
         delta = self.D[q, k + 1:].clone()
         kc = self.K[q].cpu().numpy()
         fracs = np.zeros(ng + 1)
@@ -557,10 +566,38 @@ class _Overlap:
         eng.G, self.Gn = Gn, Gc
         return err, delta, fracs, targets, t_fine, t_corr
 
+    def sweep(self):
+        """Coarse sweep window by window (parareal.py:210-229; the reference's
+        default field guard), the first iteration's windows enqueued behind the
+        rows they start from, their jumps behind G(row_0[n-1]) == row_0[n]."""
+        torch, eng = self.torch, self.eng
+        ng, nx = eng.cfg.ng, eng.nx
+        R, Gc, cs = eng.row, eng.G, self.cs
+        t_host = time.perf_counter()
+        start = torch.cuda.Event(enable_timing=TIMELINE)
+        start.record(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            cs.wait_event(start)
+        for n in range(1, ng + 1):
+            with torch.cuda.stream(cs):
+                self.cdev.chain_raw(R[n - 1].view(1, nx), R[n].view(1, 1, nx), Gc[n].view(1, 1, nx),
+                                    None, None, self.sched[n], eng.fluid_p.dt, eng.be.rb1,
+                                    SOLVABILITY_RTOL)
+                self.ev_row[n].record(cs)
+            if eng.cfg.k_max > 0:
+                self._fine(0, n, R[n - 1], start if n == 1 else self.ev_row[n - 1])
+                self._jump(0, n, Gc[n], self.ev_row[n])
+        self.spec = 0 if eng.cfg.k_max > 0 else None
+        self.sweep_enqueue_s = time.perf_counter() - t_host
+        self.cdev.check_stream(cs)
+        if TIMELINE:
+            self.sweep_timeline = [(n, start.elapsed_time(self.ev_fstart[0][n]),
+                                    start.elapsed_time(self.ev_row[n])) for n in range(1, ng + 1)]
+            self.sweep_wait_s = time.perf_counter() - t_host
+
     def sync(self):
         for pair in self.fs[1:]:
-            for s in pair:
-                s.synchronize()
+            pair[0].synchronize()
         self.cs.synchronize()
         self.spec = None
 
@@ -618,7 +655,11 @@ def coarse_sweep(rho0, cfg: PararealConfig, fluid_p: FluidStepParams, mesh: Phas
     if g0 is None:
         g0 = np.zeros((mesh.nx,) + mesh.vgrid.shape)
     eng = _Engine(cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p, backend=_BACKEND)
-    eng.coarse_sweep()
+    if eng.comm.size == 1 and isinstance(eng.be, DeviceBackend) and OVERLAP:
+        eng.overlap = _Overlap.get(eng)
+        eng.overlap.sweep()     # also starts iteration 0's windows
+    else:
+        eng.coarse_sweep()
     _ENGINES[id(ledger)] = eng
     ledger.rho.append(eng.row.cpu().numpy())
     ledger.kinetic_fraction = np.zeros(cfg.ng + 1)

@@ -32,6 +32,10 @@ def main():
         ov = getattr(parareal, "_Overlap", None)
         for o in (ov._cache.values() if ov else []):
             print("   last iteration host enqueue %.2f ms" % (getattr(o, "host_enqueue_s", 0) * 1e3))
+            print("   sweep enqueue %.2f ms, until swept %.2f ms" % (
+                getattr(o, "sweep_enqueue_s", 0) * 1e3, getattr(o, "sweep_wait_s", 0) * 1e3))
+            for n, fs, cr in getattr(o, "sweep_timeline", []):
+                print(f"      sweep window {n:2d}: row ready {cr:7.2f} ms, its F starts {fs:7.2f} ms")
             for n, fs, fe, cr in getattr(o, "timeline", []):
                 print(f"      window {n:2d}: F {fs:7.2f} .. {fe:7.2f} ms, corrected at {cr:7.2f} ms")
         for it in tm.iterations:
