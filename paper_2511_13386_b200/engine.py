@@ -94,13 +94,18 @@ def make_phase(mesh: PhaseMesh, eps_list, dt_list, nsteps_list) -> Phase:
     cm = np.empty((B, nx))
     cflu = np.empty(B)
     dts = np.empty(B)
+    rows = {}  # slices sharing (eps, dt) share their coefficient rows
     for b in range(B):
         dt = float(dt_list[b])
         dts[b] = dt
-        e = eps_rows(eps_list[b], nx)
-        k1[b] = per_value(e, lambda v: relaxation_coefficients(dt, v)[0])
-        k2[b] = per_value(e, lambda v: relaxation_coefficients(dt, v)[1])
-        cm[b] = per_value(e, lambda v: dt / (v * dx))
+        eb = eps_list[b]
+        key = (id(eb) if hasattr(eb, "iface") else float(eb), dt)
+        if key not in rows:
+            e = eps_rows(eb, nx)
+            rows[key] = (per_value(e, lambda v: relaxation_coefficients(dt, v)[0]),
+                         per_value(e, lambda v: relaxation_coefficients(dt, v)[1]),
+                         per_value(e, lambda v: dt / (v * dx)))
+        k1[b], k2[b], cm[b] = rows[key]
         cflu[b] = m2 * (dt / dx)
     def uniform(a):  # per slice: the common value of a row, else NaN
         return np.array([row[0] if (row == row[0]).all() else np.nan for row in a])
