@@ -47,14 +47,15 @@ typedef struct pk_ctx pk_ctx;
  * arrays are HOST pointers holding the reference's own build_mesh values
  * (mesh.py:197-236), uploaded verbatim. */
 typedef struct pk_mesh {
-  int32_t nx, nv;
+  int32_t nx, nv;        /* nv: velocity nodes per interface row, nvx * nvy * nvz */
   double dx, dvx, dv3, m0, m2, x_star, v_star;
-  const double* vx;      /* host [nv] */
+  const double* vx;      /* host [nv]  xi of every node of the row (vx[jx] repeated nvy*nvz times) */
   const double* M;       /* host [nv] */
   const double* xi_M;    /* host [nv]  vx * M            (mesh.py:167) */
   const double* w2;      /* host [nv]  (vx**2 - 1) * M   (lifting.py:88) */
   double stencil[4][7];  /* adaptation.py:29-34, as Python floats */
   double stencil_scale[4]; /* dx ** -order (adaptation.py:51) */
+  int32_t nvyz;          /* nvy * nvz: stride of the xi axis in a row (1: 1D-x/1D-v) */
 } pk_mesh;
 
 /* One run of identical steps.  Device arrays, per slice b (and per

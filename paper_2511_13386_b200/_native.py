@@ -28,6 +28,7 @@ class PkMesh(C.Structure):
         ("m2", C.c_double), ("x_star", C.c_double), ("v_star", C.c_double),
         ("vx", c_double_p), ("M", c_double_p), ("xi_M", c_double_p), ("w2", c_double_p),
         ("stencil", (C.c_double * 7) * 4), ("stencil_scale", C.c_double * 4),
+        ("nvyz", C.c_int32),
     ]
 
 

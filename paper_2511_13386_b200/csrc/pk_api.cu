@@ -183,6 +183,9 @@ int32_t pk_debug_profile(pk_ctx* c, void* dev_counters) {
 
 pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   if (!mesh || mesh->nx < 7 || mesh->nv < 1) return nullptr;
+  const int nvyz = mesh->nvyz > 0 ? mesh->nvyz : 1;
+  // 1D-3V rows run on the generic layout: one warp per row (<= 256 nodes)
+  if (mesh->nv % nvyz != 0 || (nvyz > 1 && mesh->nv > 256)) return nullptr;
   pk_ctx* c = new pk_ctx();
   c->device = device;
   if (cudaSetDevice(device) != cudaSuccess) {
@@ -194,6 +197,7 @@ pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   pk::MeshDev& m = c->m;
   m.nx = nx;
   m.nv = nv;
+  m.nvyz = nvyz;
   m.dx = mesh->dx;
   m.rdx = 1.0 / mesh->dx;
   m.two_dx = 2.0 * mesh->dx;

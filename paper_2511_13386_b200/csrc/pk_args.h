@@ -11,6 +11,7 @@ namespace pk {
 // uploaded verbatim: mesh.py:167,211-235; lifting.py:88).
 struct MeshDev {
   int nx, nv;
+  int nvyz;            // nvy * nvz: stride of the xi axis within a row (1: 1D-x/1D-v)
   double dx, rdx, two_dx, dvx, dv3, m0, m2;
   double three_rb_unused;
   const double* vx;    // [nv] velocity centres xi_j

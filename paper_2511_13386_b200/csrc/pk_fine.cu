@@ -1438,10 +1438,10 @@ __device__ void micro_phase_gen(const FineArgs& a, const SliceView& v, const Sme
     rc.k1 = P.k1[o + i];
     rc.k2 = P.k2[o + i];
     double out[GT];
-    gen_micro(gp, gc, gn, out, sm.vx, sm.M, sm.xiM, rc, nv, m.dx, m.rdx, lane);
+    gen_micro(gp, gc, gn, out, sm.vx, sm.M, sm.xiM, rc, nv, m.nvyz, wrow, m.dx, m.rdx, lane);
     gen_store(out, gout + (size_t)i * nv, lane, nv);
     double bx, bsq;
-    gen_moments(out, sm, nv, m.dv3, wrow, lane, bx, bsq);
+    gen_moments(out, sm, nv, m.nvyz, m.dv3, wrow, lane, bx, bsq);
     if (lane == 0) {
       v.fl_w[i] = bx;
       v.sq_w[i] = bsq;
@@ -1934,6 +1934,7 @@ static cudaError_t launch_lift_T(const LiftArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_lift(const LiftArgs& a, cudaStream_t st) {
+  if (a.m.nvyz > 1) return a.m.nv <= 32 * GT ? launch_lift_T<0>(a, st) : cudaErrorInvalidValue;
   switch (a.m.nv) {
     case 64: return launch_lift_T<2>(a, st);
     case 128: return launch_lift_T<4>(a, st);
@@ -1956,6 +1957,10 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
+  if (a.m.nvyz > 1) {  // 1D-3V rows: the generic layout (fast layouts assume one xi axis)
+    if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
+    return cudaErrorInvalidValue;
+  }
   switch (a.m.nv) {
     // producer/consumer GS pipeline: 7 consumer warps + 1 producer warp
     case 64: return launch_T<2, 16, 4, 128>(a, C, st);   // G8 per-warp rings, 4 warps

@@ -151,7 +151,9 @@ __device__ __forceinline__ void fast_micro(const double (&gp)[T], const double (
 
 // ---------------------------------------------------------------------------
 // Generic layout (any nv <= 256): lane l, slot s holds column 32 s + l.  The
-// fold and the pairwise sum go through a per-warp shared-memory row.
+// fold and the pairwise sum go through a per-warp shared-memory row.  A row is
+// (nvx, nvy, nvz) in C order; S = nvy * nvz is the stride of the xi axis
+// (S = 1: the 1D-x/1D-v reduction).
 constexpr int GT = 8;  // slots: nv <= 256
 
 __device__ __forceinline__ void gen_load(double (&v)[GT], const double* row, int lane, int nv) {
@@ -170,31 +172,38 @@ __device__ __forceinline__ void gen_store(const double (&v)[GT], double* row, in
   }
 }
 
+// <q>: fold the xi mirror pairs (jx, nvx-1-jx) of every (vy, vz) column, one
+// pairwise sum over the folded (nvx/2, nvy, nvz) block in memory order, plus
+// the middle xi plane's own pairwise sum for odd nvx (mesh.py:95-133; numpy
+// reduces the trailing contiguous axes as one flattened pairwise sum).  The
+// folded block has nv/2 <= 128 terms: one leaf.
 __device__ __forceinline__ double gen_bracket(const double (&q)[GT], double* wrow, int lane,
-                                              int nv, double dv3) {
+                                              int nv, int S, double dv3) {
 #pragma unroll
   for (int s = 0; s < GT; ++s) {
     const int c = 32 * s + lane;
     if (c < nv) wrow[c] = q[s];
   }
   __syncwarp();
-  const int h = nv / 2;
-  double mid = (nv & 1) ? wrow[h] : 0.0;
+  const int nvx = nv / S, h = nvx / 2, F = h * S;
+  // the middle plane [F, F + S) is never overwritten below
+  const double mid = (nvx & 1) ? warp_leaf([&](int j) { return wrow[j]; }, F, S, lane) : 0.0;
   double f[GT];
 #pragma unroll
   for (int s = 0; s < GT; ++s) {
     const int j = 32 * s + lane;
-    f[s] = j < h ? wrow[j] + wrow[nv - 1 - j] : 0.0;
+    const int jx = j / S;
+    f[s] = j < F ? wrow[j] + wrow[(nvx - 1 - jx) * S + (j - jx * S)] : 0.0;
   }
   __syncwarp();
 #pragma unroll
   for (int s = 0; s < GT; ++s) {
     const int j = 32 * s + lane;
-    if (j < h) wrow[j] = f[s];
+    if (j < F) wrow[j] = f[s];
   }
   __syncwarp();
-  double tot = warp_leaf([&](int j) { return wrow[j]; }, 0, h, lane);
-  if (nv & 1) tot = tot + mid;
+  double tot = warp_leaf([&](int j) { return wrow[j]; }, 0, F, lane);
+  if (nvx & 1) tot = tot + mid;
   __syncwarp();
   return tot * dv3;
 }
@@ -202,25 +211,37 @@ __device__ __forceinline__ double gen_bracket(const double (&q)[GT], double* wro
 __device__ __forceinline__ void gen_micro(const double (&gp)[GT], const double (&gc)[GT],
                                           const double (&gn)[GT], double (&out)[GT],
                                           const double* svx, const double* sM, const double* sxiM,
-                                          const RowCoef& rc, int nv, double dx, double rdx,
-                                          int lane) {
-  double left[GT], right[GT];
-#pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const double u = __shfl_sync(FULL, gc[s], (lane + 31) & 31);
-    const double d = __shfl_sync(FULL, gc[s], (lane + 1) & 31);
-    left[s] = u;
-    right[s] = d;
-  }
+                                          const RowCoef& rc, int nv, int S, double* wrow,
+                                          double dx, double rdx, int lane) {
+  // xi neighbours (c - S, c + S); edge planes have zero inflow (kinetic.py:176-187)
   double lfix[GT], rfix[GT];
+  if (S == 1) {  // neighbouring lanes: shuffles
+    double left[GT], right[GT];
 #pragma unroll
-  for (int s = 0; s < GT; ++s) {
-    const int c = 32 * s + lane;
-    // column c-1 for lane 0 is lane 31 of slot s-1; column c+1 for lane 31 is lane 0 of slot s+1
-    lfix[s] = lane >= 1 ? left[s] : (s >= 1 ? left[s >= 1 ? s - 1 : 0] : 0.0);
-    rfix[s] = lane <= 30 ? right[s] : (s + 1 < GT ? right[s + 1 < GT ? s + 1 : 0] : 0.0);
-    if (c == 0) lfix[s] = 0.0;
-    if (c + 1 >= nv) rfix[s] = 0.0;
+    for (int s = 0; s < GT; ++s) {
+      left[s] = __shfl_sync(FULL, gc[s], (lane + 31) & 31);
+      right[s] = __shfl_sync(FULL, gc[s], (lane + 1) & 31);
+    }
+#pragma unroll
+    for (int s = 0; s < GT; ++s) {
+      // column c-1 for lane 0 is lane 31 of slot s-1; column c+1 for lane 31 is lane 0 of slot s+1
+      lfix[s] = lane >= 1 ? left[s] : (s >= 1 ? left[s >= 1 ? s - 1 : 0] : 0.0);
+      rfix[s] = lane <= 30 ? right[s] : (s + 1 < GT ? right[s + 1 < GT ? s + 1 : 0] : 0.0);
+    }
+  } else {  // 1D-3V: through the warp's shared row
+#pragma unroll
+    for (int s = 0; s < GT; ++s) {
+      const int c = 32 * s + lane;
+      if (c < nv) wrow[c] = gc[s];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < GT; ++s) {
+      const int c = 32 * s + lane;
+      lfix[s] = c >= S && c < nv ? wrow[c - S] : 0.0;
+      rfix[s] = c + S < nv ? wrow[c + S] : 0.0;
+    }
+    __syncwarp();
   }
   const double Ep = rc.vsg > 0 ? rc.vco : 0.0;
   const double Em = rc.vsg < 0 ? rc.vco : 0.0;
@@ -239,9 +260,9 @@ __device__ __forceinline__ void gen_micro(const double (&gp)[GT], const double (
     o = o + xm * (gn[s] - g);
     o = qdiv(o, dx, rdx);
     // literal reference terms (both signs) for the generic path
-    const double dm = (c == 0) ? g : g - lfix[s];
+    const double dm = (c < S) ? g : g - lfix[s];
     o = o + dm * Ep;
-    const double dp = (c == nv - 1) ? -g : rfix[s] - g;
+    const double dp = (c >= nv - S) ? -g : rfix[s] - g;
     o = o + dp * Em;
     o = o - sM[c] * rc.dc;
     const double forcing = o + sxiM[c] * rc.J;
@@ -303,7 +324,7 @@ __device__ void gen_lift_row(double (&g)[GT], const LiftRow& L, int order, int h
   }
   if (project) {
     for (int pass = 0; pass < 2; ++pass) {
-      const double bb = gen_bracket(g, wrow, lane, nv, m.dv3) / m.m0;
+      const double bb = gen_bracket(g, wrow, lane, nv, m.nvyz, m.dv3) / m.m0;
 #pragma unroll
       for (int s = 0; s < GT; ++s) {
         const int c = 32 * s + lane;
@@ -327,7 +348,7 @@ __device__ __forceinline__ void fast_moments(const double (&g)[T], const Smem& s
   bsq = fast_bracket<T>(r, lane, dv3);
 }
 
-__device__ __forceinline__ void gen_moments(const double (&g)[GT], const Smem& sm, int nv,
+__device__ __forceinline__ void gen_moments(const double (&g)[GT], const Smem& sm, int nv, int S,
                                             double dv3, double* wrow, int lane, double& bx,
                                             double& bsq) {
   double q[GT], r[GT];
@@ -337,8 +358,8 @@ __device__ __forceinline__ void gen_moments(const double (&g)[GT], const Smem& s
     q[s] = c < nv ? sm.vx[c] * g[s] : 0.0;
     r[s] = g[s] * g[s];
   }
-  bx = gen_bracket(q, wrow, lane, nv, dv3);
-  bsq = gen_bracket(r, wrow, lane, nv, dv3);
+  bx = gen_bracket(q, wrow, lane, nv, S, dv3);
+  bsq = gen_bracket(r, wrow, lane, nv, S, dv3);
 }
 
 // Layout dispatch: T == 0 selects the generic layout.
@@ -373,7 +394,7 @@ template <int T>
 __device__ __forceinline__ void row_moments(const double (&g)[Layout<T>::S], const Smem& sm,
                                             const MeshDev& m, double* wrow, int lane, double& bx,
                                             double& bsq) {
-  if constexpr (T == 0) gen_moments(g, sm, m.nv, m.dv3, wrow, lane, bx, bsq);
+  if constexpr (T == 0) gen_moments(g, sm, m.nv, m.nvyz, m.dv3, wrow, lane, bx, bsq);
   else fast_moments<T>(g, sm, m.dv3, lane, bx, bsq);
 }
 

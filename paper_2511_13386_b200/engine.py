@@ -162,7 +162,8 @@ class Device:
         self.nx = mesh.nx
         self.nv = mesh.nv
         grid = mesh.vgrid
-        vx = np.ascontiguousarray(grid.vx, dtype=float)
+        # xi of every node of a row: (nvx, nvy, nvz) in C order
+        vx = np.ascontiguousarray(np.repeat(np.asarray(grid.vx, dtype=float), mesh.nvyz))
         M = np.ascontiguousarray(grid.M.reshape(-1))
         xiM = np.ascontiguousarray(mesh.xi_M.reshape(-1))
         w2 = np.ascontiguousarray(((grid.xi**2 - 1.0) * grid.M).reshape(-1))
@@ -177,6 +178,7 @@ class Device:
             for o in range(7):
                 m.stencil[p][o] = STENCIL_COEFFS[p + 1][o]
             m.stencil_scale[p] = mesh.dx ** (-(p + 1))
+        m.nvyz = mesh.nvyz
         with torch.cuda.device(self.device):
             torch.cuda.init()
             self.ctx = self.lib.pk_create(self.device.index or 0, C.byref(m))

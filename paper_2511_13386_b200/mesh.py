@@ -3,9 +3,12 @@
 The mesh is built on the host with numpy exactly as the reference builds it
 (mirrored velocity centres, Maxwellian renormalised twice by the folded
 bracket), and its velocity constants are uploaded verbatim to the device by
-:mod:`paper_2511_13386_b200.engine`.  This build covers 1D-x / 1D-v grids
-(``nvy == nvz == 1``: exact reduction of the reference's 1D-3V
-grid); arrays keep the reference's shapes, ``g`` is ``(nx, nvx, 1, 1)``.
+:mod:`paper_2511_13386_b200.engine`.  Two grid families: the reference's
+1D-3V tensor grids (``nvy, nvz >= 4``, mesh.py:58-65) and the 1D-x/1D-v
+reduction ``nvy == nvz == 1`` (exact, same arrays and arithmetic
+with trivial vy/vz axes).  Arrays keep the reference's shapes: ``g`` is
+``(nx, nvx, nvy, nvz)``; the device row of an interface is its
+``nv = nvx * nvy * nvz`` values in that (C) order.
 """
 
 from __future__ import annotations
@@ -36,7 +39,8 @@ def _centers(n: int, v_star: float) -> np.ndarray:
 
 @dataclass(frozen=True)
 class MeshSpec:
-    """Grid counts and domain sizes (mesh.py:47-65).  ``nvy = nvz = 1``."""
+    """Grid counts and domain sizes (mesh.py:47-65); ``nvy = nvz = 1`` selects
+    the 1D-x/1D-v reduction."""
 
     nx: int
     nvx: int
@@ -51,20 +55,23 @@ class MeshSpec:
         if self.nvx < 4:
             raise MeshTooSmall(f"nvx={self.nvx}: velocity grids need at least 4 cells")
         if (self.nvy, self.nvz) != (1, 1):
-            raise NotImplementedError(
-                "this build implements the 1D-x/1D-v reduction (nvy = nvz = 1); "
-                "1D-3V grids are the SURVEY §8(f) item 4 extension")
+            for name, n in (("nvy", self.nvy), ("nvz", self.nvz)):
+                if n < 4:
+                    raise MeshTooSmall(f"{name}={n}: velocity grids need at least 4 cells")
         if self.x_star <= 0.0 or self.v_star <= 0.0:
             raise ValueError("x_star and v_star must be positive")
 
 
 def _fold_sum(q: np.ndarray) -> np.ndarray:
-    """Mirror-pair fold along axis -1, numpy pairwise sum (mesh.py:95-133)."""
-    n = q.shape[-1]
+    """<.> of (..., nvx, nvy, nvz) arrays without dv3 (mesh.py:95-133): fold the
+    xi mirror pairs, numpy-sum the folded block over the three velocity axes
+    (one pairwise sum over the flattened (nvx/2, nvy, nvz) block), plus the
+    middle xi plane summed over (nvy, nvz) for odd nvx."""
+    n = q.shape[-3]
     h = n // 2
-    tot = (q[..., :h] + q[..., ::-1][..., :h]).sum(axis=-1)
+    tot = (q[..., :h, :, :] + q[..., ::-1, :, :][..., :h, :, :]).sum(axis=(-3, -2, -1))
     if n % 2 == 1:
-        tot = tot + q[..., h]
+        tot = tot + q[..., h, :, :].sum(axis=(-2, -1))
     return tot
 
 
@@ -75,7 +82,7 @@ class VelocityGrid:
     vz: np.ndarray
     dvx: float
     dv3: float
-    M: np.ndarray          # (nvx, 1, 1)
+    M: np.ndarray          # (nvx, nvy, nvz)
     xi: np.ndarray         # (nvx, 1, 1)
     m0: float
     m2: float
@@ -90,14 +97,14 @@ def bracket(q: np.ndarray, grid: VelocityGrid) -> float:
     """<q> over the whole velocity grid (mesh.py:112-121)."""
     if q.shape != grid.shape:
         raise ValueError(f"expected shape {grid.shape}, got {q.shape}")
-    return float(_fold_sum(q.reshape(-1)) * grid.dv3)
+    return float(_fold_sum(q) * grid.dv3)
 
 
 def bracket_staggered(q: np.ndarray, grid: VelocityGrid) -> np.ndarray:
-    """Per-interface <q> of a (..., nvx, 1, 1) field (mesh.py:124-133)."""
+    """Per-interface <q> of a (..., nvx, nvy, nvz) field (mesh.py:124-133)."""
     if q.shape[-3:] != grid.shape:
         raise ValueError(f"expected trailing shape {grid.shape}, got {q.shape}")
-    return _fold_sum(q.reshape(q.shape[:-3] + (q.shape[-3],))) * grid.dv3
+    return _fold_sum(q) * grid.dv3
 
 
 @dataclass(frozen=True)
@@ -130,7 +137,17 @@ class PhaseMesh:
 
     @property
     def nv(self) -> int:
+        """Velocity nodes per interface row (nvx * nvy * nvz)."""
+        return int(self.vgrid.M.size)
+
+    @property
+    def nvx(self) -> int:
         return self.vgrid.vx.shape[0]
+
+    @property
+    def nvyz(self) -> int:
+        """Row stride of the xi axis (nvy * nvz; 1 for the 1D-x/1D-v reduction)."""
+        return self.nv // self.nvx
 
     def bracket(self, q):
         return bracket(q, self.vgrid)

@@ -276,7 +276,7 @@ class _Engine:
         self.comm = comm or _Comm()
         self.rho_bar = float(rho_bar)
         self.g0 = g0
-        self.nx, self.nv, ng = mesh.nx, mesh.vgrid.vx.shape[0], cfg.ng
+        self.nx, self.nv, ng = mesh.nx, mesh.nv, cfg.ng
         b = cfg.boundaries
         self.sc = [substep_sizes(float(b[n - 1]), float(b[n]), fluid_p.dt) for n in range(1, ng + 1)]
         self.sf = [substep_sizes(float(b[n - 1]), float(b[n]), kin_p.dt) for n in range(1, ng + 1)]

@@ -34,8 +34,10 @@ def test_mesh_validation():
         pk.build_mesh(pk.MeshSpec(nx=6, nvx=8))
     with pytest.raises(pk.MeshTooSmall):
         pk.build_mesh(pk.MeshSpec(nx=16, nvx=3))
-    with pytest.raises(NotImplementedError):
-        pk.build_mesh(pk.MeshSpec(nx=16, nvx=8, nvy=4, nvz=4))
+    with pytest.raises(pk.MeshTooSmall):  # 3V grids follow the reference's >= 4 rule
+        pk.build_mesh(pk.MeshSpec(nx=16, nvx=8, nvy=2, nvz=4))
+    m3 = pk.build_mesh(pk.MeshSpec(nx=16, nvx=8, nvy=4, nvz=4))
+    assert m3.vgrid.shape == (8, 4, 4) and (m3.nv, m3.nvx, m3.nvyz) == (128, 8, 16)
     with pytest.raises(ValueError):
         pk.build_mesh(pk.MeshSpec(nx=16, nvx=8, v_star=-1.0))
 
