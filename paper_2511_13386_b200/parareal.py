@@ -372,18 +372,7 @@ class _Engine:
 # single GPU (tests can switch it off to compare the two schedules).
 OVERLAP = True
 TIMELINE = False    # diagnostics: record per-window event times (tools/par_timing.py)
-_DEVICE_POOLS: dict = {}
-
-
-def _device_pool(mesh, device, ng):
-    """Two solver contexts per window (one per iteration parity) plus one for
-    the correction, cached per (mesh, device, ng)."""
-    key = (id(mesh), str(device), ng)
-    pool = _DEVICE_POOLS.get(key)
-    if pool is None or pool[0] is not mesh:
-        devs = [None] + [[Device(mesh, device), Device(mesh, device)] for _ in range(ng)]
-        pool = _DEVICE_POOLS[key] = (mesh, devs, Device(mesh, device))
-    return pool[1], pool[2]
+OVERLAP_CACHE = 2   # schedules (with their contexts and buffers) kept for reuse
 
 
 class _Overlap:
@@ -402,19 +391,25 @@ class _Overlap:
     in the phase-by-phase schedule, so ledgers are bitwise identical; the
     speculative work of an iteration that never happens is dropped unread."""
 
-    _cache: dict = {}
+    _cache: dict = {}   # insertion-ordered: least recently used first
 
     @classmethod
     def get(cls, eng):
         """Resources are cached per (mesh, device, schedule, parameters): a
-        repeated run reuses the prepared phases, buffers and streams."""
+        repeated run reuses the solver contexts, prepared phases, buffers and
+        streams.  At most OVERLAP_CACHE schedules are kept; an evicted one is
+        synchronised before its contexts and buffers are released."""
         cfg = eng.cfg
         key = (id(eng.mesh), str(eng.be.device), cfg.ng, id(cfg.eps), eng.kin_p.dt,
                eng.fluid_p.dt, eng.fluid_p.m2, eng.rtol_f, repr(eng.knobs), tuple(eng.sf),
                tuple(eng.sc))
-        ov = cls._cache.get(key)
+        ov = cls._cache.pop(key, None)
         if ov is None or ov.mesh is not eng.mesh or ov.eps is not cfg.eps:
-            ov = cls._cache[key] = cls(eng)
+            ov = cls(eng)
+        cls._cache[key] = ov
+        while len(cls._cache) > max(1, OVERLAP_CACHE):
+            old = cls._cache.pop(next(iter(cls._cache)))
+            old.sync()
         ov.sync()
         ov.eng = eng
         ov.Rn = eng.torch.empty_like(eng.row)
@@ -428,7 +423,9 @@ class _Overlap:
         cfg, mesh, be = eng.cfg, eng.mesh, eng.be
         ng, nx, nv = cfg.ng, eng.nx, eng.nv
         dv = be.device
-        self.devs, self.cdev = _device_pool(mesh, dv, ng)
+        # two solver contexts per window (one per iteration parity) + the correction's
+        self.devs = [None] + [[Device(mesh, dv), Device(mesh, dv)] for _ in range(ng)]
+        self.cdev = Device(mesh, dv)
         # torch hands out streams from a pool of 32 per priority: the
         # correction (the critical path) takes a high-priority stream of its
         # own; each window one low-priority stream for both parities (windows
