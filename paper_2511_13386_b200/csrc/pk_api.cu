@@ -30,7 +30,7 @@ struct pk_ctx {
   int num_sms = 148;
   pk::MeshDev m{};
   double* d_const = nullptr;  // vx | M | xiM | w2
-  PwPlan* d_plan = nullptr;
+  PwPlan* d_plan = nullptr;  // [x: nx terms, folded velocity row, middle xi plane]
   pk::Status* d_status = nullptr;
   int cap = 0;
   // workspace
@@ -184,8 +184,7 @@ int32_t pk_debug_profile(pk_ctx* c, void* dev_counters) {
 pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   if (!mesh || mesh->nx < 7 || mesh->nv < 1) return nullptr;
   const int nvyz = mesh->nvyz > 0 ? mesh->nvyz : 1;
-  // 1D-3V rows run on the generic layout: one warp per row (<= 256 nodes)
-  if (mesh->nv % nvyz != 0 || (nvyz > 1 && mesh->nv > 256)) return nullptr;
+  if (mesh->nv % nvyz != 0) return nullptr;
   pk_ctx* c = new pk_ctx();
   c->device = device;
   if (cudaSetDevice(device) != cudaSuccess) {
@@ -212,25 +211,31 @@ pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   std::memcpy(h.data() + nv, mesh->M, nv * 8);
   std::memcpy(h.data() + 2 * nv, mesh->xi_M, nv * 8);
   std::memcpy(h.data() + 3 * nv, mesh->w2, nv * 8);
-  PwPlan plan;
-  if (!build_plan(nx, &plan)) {
+  // pairwise plans: x sums (nx terms), and for 1D-3V rows the folded velocity
+  // block ((nvx/2) nvy nvz terms) and the middle xi plane (nvy nvz terms)
+  PwPlan plan[3];
+  const int nvx = nv / nvyz;
+  if (!build_plan(nx, &plan[0]) || !build_plan((nvx / 2) * nvyz, &plan[1]) ||
+      !build_plan(nvyz, &plan[2])) {
     delete c;
     return nullptr;
   }
   if (cudaMalloc(&c->d_const, h.size() * 8) != cudaSuccess ||
-      cudaMalloc(&c->d_plan, sizeof(PwPlan)) != cudaSuccess ||
+      cudaMalloc(&c->d_plan, 3 * sizeof(PwPlan)) != cudaSuccess ||
       cudaMalloc(&c->d_status, sizeof(pk::Status)) != cudaSuccess) {
     delete c;
     return nullptr;
   }
   cudaMemcpy(c->d_const, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(c->d_plan, &plan, sizeof(PwPlan), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->d_plan, plan, 3 * sizeof(PwPlan), cudaMemcpyHostToDevice);
   cudaMemset(c->d_status, 0, sizeof(pk::Status));
   m.vx = c->d_const;
   m.M = c->d_const + nv;
   m.xiM = c->d_const + 2 * nv;
   m.w2 = c->d_const + 3 * nv;
   m.plan_x = c->d_plan;
+  m.plan_f = c->d_plan + 1;
+  m.plan_s = c->d_plan + 2;
   return c;
 }
 
@@ -292,7 +297,9 @@ int32_t pk_fine_propagate(pk_ctx* c, int32_t B, double* rho, double* E, double* 
       !rho_bar)
     return fail(c, PK_ERR_BAD_ARG, "pk_fine_propagate: null argument");
   const int nv = c->m.nv;
-  if (!(nv == 64 || nv == 128 || nv == 256 || nv == 512 || nv <= 256))
+  // 1V rows: the fast layouts (64/128/256/512) or the generic one (<= 256);
+  // 1D-3V rows of any length (generic up to 256 nodes, big rows beyond)
+  if (c->m.nvyz == 1 && !(nv == 512 || nv <= 256))
     return fail(c, PK_ERR_UNSUPPORTED, "pk_fine_propagate: nv not supported");
   cudaSetDevice(c->device);
   int r = ensure(c, B);

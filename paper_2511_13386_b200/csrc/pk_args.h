@@ -21,6 +21,8 @@ struct MeshDev {
   double stc[4][7];    // 7-point stencil coefficients, offsets -3..3 (adaptation.py:29-34)
   double sts[4];       // dx ** (-order)
   const PwPlan* plan_x;  // pairwise plan for nx-term reductions
+  const PwPlan* plan_f;  // folded velocity row ((nvx/2) * nvyz terms)   (big rows)
+  const PwPlan* plan_s;  // middle xi plane (nvyz terms, odd nvx)        (big rows)
 };
 
 // One run of identical steps, per slice.

@@ -25,6 +25,7 @@
 
 #include "../../include/pk.h"
 #include "pk_rows.cuh"
+#include "pk_big.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -601,11 +602,18 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
         L.e2 = a.eps2[o];
         L.drift = v.tE[i];
         L.Rif = v.tA[i];
-        double g[Layout<T>::S];
-        row_lift<T>(g, L, a.lift_order, a.time_elim == 1, 1, sm, m, sm.wrow + warp * nv, lane);
-        row_store<T>(g, gin + (size_t)i * nv, lane, nv);
         double bx, bsq;
-        row_moments<T>(g, sm, m, sm.wrow + warp * nv, lane, bx, bsq);
+        if constexpr (T < 0) {
+          double* row = gin + (size_t)i * nv;
+          double* scr = sm.wrow + warp * BIG_SCR;
+          big_row_lift(row, L, a.lift_order, a.time_elim == 1, 1, m, scr, lane);
+          big_row_moments(row, m, scr, false, bx, bsq);
+        } else {
+          double g[Layout<T>::S];
+          row_lift<T>(g, L, a.lift_order, a.time_elim == 1, 1, sm, m, sm.wrow + warp * nv, lane);
+          row_store<T>(g, gin + (size_t)i * nv, lane, nv);
+          row_moments<T>(g, sm, m, sm.wrow + warp * nv, lane, bx, bsq);
+        }
         if (lane == 0) v.blift[i] = bx;
       }
     } else if (a.reinit == 1) {
@@ -1449,6 +1457,40 @@ __device__ void micro_phase_gen(const FineArgs& a, const SliceView& v, const Sme
   }
 }
 
+// Micro phase, big rows (pk_big.cuh): one warp per listed row.
+__device__ void micro_phase_big(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
+                                const double* gin, double* gout, int wg, int nwg) {
+  const MeshDev& m = a.m;
+  const int nx = m.nx, nv = m.nv;
+  const int lane = threadIdx.x & 31;
+  const int nk = __ldcg(v.nk);
+  const bool dense = nk == nx;
+  const int p0 = (int)(((long long)wg * nk) / nwg);
+  const int p1 = (int)(((long long)(wg + 1) * nk) / nwg);
+  const PhaseDev& P = a.ph[ph];
+  const size_t o = (size_t)v.b * nx;
+  double* scr = sm.wrow + (threadIdx.x >> 5) * BIG_SCR;
+  for (int p = p0; p < p1; ++p) {
+    const int i = dense ? p : __ldcg(v.klist + p);
+    RowCoef rc;
+    rc.vsg = __ldcg(v.vsg + i);
+    rc.vco = __ldcg(v.vco + i);
+    rc.dc = __ldcg(v.dco + i);
+    rc.J = __ldcg(v.gJ + i);
+    rc.k1 = P.k1[o + i];
+    rc.k2 = P.k2[o + i];
+    double* row = gout + (size_t)i * nv;
+    big_micro_row(gin + (size_t)wrap(i - 1, nx) * nv, gin + (size_t)i * nv,
+                  gin + (size_t)wrap(i + 1, nx) * nv, row, m, rc, lane);
+    double bx, bsq;
+    big_row_moments(row, m, scr, a.adaptation != 0, bx, bsq);
+    if (lane == 0) {
+      v.fl_w[i] = bx;
+      v.sq_w[i] = bsq;
+    }
+  }
+}
+
 // Prologue row pass: (optionally lift and) copy the input rows into the
 // step-0 input buffer and compute their moments.
 template <int T>
@@ -1462,6 +1504,30 @@ __device__ void prologue_rows(const FineArgs& a, const SliceView& v, const Smem&
   double* wrow = sm.wrow + (threadIdx.x >> 5) * nv;
   const int p0 = (int)(((long long)wg * nx) / nwg);
   const int p1 = (int)(((long long)(wg + 1) * nx) / nwg);
+  if constexpr (T < 0) {  // big rows: work on the rows in global memory
+    double* scr = sm.wrow + (threadIdx.x >> 5) * BIG_SCR;
+    for (int i = p0; i < p1; ++i) {
+      double* row = gin0 + (size_t)i * nv;
+      if (lift) {
+        LiftRow L;
+        const size_t o = (size_t)v.b * nx + i;
+        L.negJ = a.neg_eps[o] * __ldcg(lJ + i);
+        L.e2 = a.eps2[o];
+        L.drift = __ldcg(ldrift + i);
+        L.Rif = __ldcg(lRif + i);
+        big_row_lift(row, L, a.lift_order, a.time_elim == 1, 1, m, scr, lane);
+      } else if (gin0 != v.ga) {
+        big_row_copy(v.ga + (size_t)i * nv, row, nv, lane);
+      }
+      double bx, bsq;
+      big_row_moments(row, m, scr, true, bx, bsq);
+      if (lane == 0) {
+        v.fl_w[i] = bx;
+        v.sq_w[i] = bsq;
+      }
+    }
+    return;
+  }
   for (int i = p0; i < p1; ++i) {
     double g[S];
     if (lift) {
@@ -1573,15 +1639,23 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     p += 128 * 8;
     sm.plan = reinterpret_cast<PwPlan*>(p);
     p += (sizeof(PwPlan) + 15) / 16 * 16;
-    sm.vx = reinterpret_cast<double*>(p); p += nv * 8;
-    sm.M = reinterpret_cast<double*>(p); p += nv * 8;
-    sm.xiM = reinterpret_cast<double*>(p); p += nv * 8;
-    sm.w2 = reinterpret_cast<double*>(p); p += nv * 8;
+    if (T >= 0) {  // velocity constants on chip (big rows read them from global)
+      sm.vx = reinterpret_cast<double*>(p); p += nv * 8;
+      sm.M = reinterpret_cast<double*>(p); p += nv * 8;
+      sm.xiM = reinterpret_cast<double*>(p); p += nv * 8;
+      sm.w2 = reinterpret_cast<double*>(p); p += nv * 8;
+    } else {
+      sm.vx = const_cast<double*>(m.vx);
+      sm.M = const_cast<double*>(m.M);
+      sm.xiM = const_cast<double*>(m.xiM);
+      sm.w2 = const_cast<double*>(m.w2);
+    }
     sm.red = reinterpret_cast<double*>(p); p += 2 * (MAX_LEAF + MAX_NODE) * 8;
     sm.misc = reinterpret_cast<int*>(p); p += 64 * 4;
     sm.wrow = reinterpret_cast<double*>(p);
-    if (T == 0) p += (size_t)nwpc * nv * 8;  // generic-layout row scratch
-    if (T != 0) {
+    if (T == 0) p += (size_t)nwpc * nv * 8;       // generic-layout row scratch
+    if (T < 0) p += (size_t)nwpc * BIG_SCR * 8;   // big rows: plan scratch
+    if (T > 0) {
       ring = reinterpret_cast<double*>(p);
       p += (size_t)(G < 0 ? 1 : nwpc) * S * RSN * 8;
     }
@@ -1593,14 +1667,15 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     const int* src = reinterpret_cast<const int*>(m.plan_x);
     int* dst = reinterpret_cast<int*>(sm.plan);
     for (int i = threadIdx.x; i < (int)(sizeof(PwPlan) / 4); i += blockDim.x) dst[i] = src[i];
-    for (int j = threadIdx.x; j < nv; j += blockDim.x) {
-      sm.vx[j] = m.vx[j];
-      sm.M[j] = m.M[j];
-      sm.xiM[j] = m.xiM[j];
-      sm.w2[j] = m.w2[j];
-    }
-    if (T != 0 && threadIdx.x < (G < 0 ? 2 * S : nwpc * S)) mbar_init(mbar + threadIdx.x, 1);
-    if (T != 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (T >= 0)
+      for (int j = threadIdx.x; j < nv; j += blockDim.x) {
+        sm.vx[j] = m.vx[j];
+        sm.M[j] = m.M[j];
+        sm.xiM[j] = m.xiM[j];
+        sm.w2[j] = m.w2[j];
+      }
+    if (T > 0 && threadIdx.x < (G < 0 ? 2 * S : nwpc * S)) mbar_init(mbar + threadIdx.x, 1);
+    if (T > 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
@@ -1706,10 +1781,12 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
                                             qbase);
       }
     }
-    else if constexpr (T != 0)
+    else if constexpr (T > 0)
       micro_phase_tma<T, S>(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg, ring_w, mbar_w, qbase);
-    else
+    else if constexpr (T == 0)
       micro_phase_gen(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
+    else
+      micro_phase_big(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     if (prof) { c1 = clock64(); tp[0] += c1 - c0; c0 = c1; }
     cluster_barrier(C);
     if (prof) { c1 = clock64(); tp[1] += c1 - c0; c0 = c1; }
@@ -1774,20 +1851,25 @@ __global__ void __launch_bounds__(256) lift_kernel(const LiftArgs a) {
   {
     unsigned char* p = smem_raw;
     sm.plan = nullptr;
-    sm.vx = reinterpret_cast<double*>(p); p += nv * 8;
-    sm.M = reinterpret_cast<double*>(p); p += nv * 8;
-    sm.xiM = reinterpret_cast<double*>(p); p += nv * 8;
-    sm.w2 = reinterpret_cast<double*>(p); p += nv * 8;
-    sm.wrow = reinterpret_cast<double*>(p); p += (blockDim.x >> 5) * nv * 8;
     sm.red = nullptr;
     sm.misc = nullptr;
+    if (T >= 0) {
+      sm.vx = reinterpret_cast<double*>(p); p += nv * 8;
+      sm.M = reinterpret_cast<double*>(p); p += nv * 8;
+      sm.xiM = reinterpret_cast<double*>(p); p += nv * 8;
+      sm.w2 = reinterpret_cast<double*>(p); p += nv * 8;
+      sm.wrow = reinterpret_cast<double*>(p); p += (blockDim.x >> 5) * nv * 8;
+    } else {  // big rows: constants from global, per-warp plan scratch only
+      sm.wrow = reinterpret_cast<double*>(p);
+    }
   }
-  for (int j = tid; j < nv; j += nt) {
-    sm.vx[j] = m.vx[j];
-    sm.M[j] = m.M[j];
-    sm.xiM[j] = m.xiM[j];
-    sm.w2[j] = m.w2[j];
-  }
+  if (T >= 0)
+    for (int j = tid; j < nv; j += nt) {
+      sm.vx[j] = m.vx[j];
+      sm.M[j] = m.M[j];
+      sm.xiM[j] = m.xiM[j];
+      sm.w2[j] = m.w2[j];
+    }
   const size_t o = (size_t)b * nx;
   const double* rho = a.rho + o;
   const double* E = a.E + o;
@@ -1830,9 +1912,14 @@ __global__ void __launch_bounds__(256) lift_kernel(const LiftArgs a) {
     L.e2 = a.eps2[o + i];
     L.drift = a.order >= 2 ? drift[i] : 0.0;
     L.Rif = a.order >= 2 ? Rif[i] : 0.0;
-    double g[Layout<T>::S];
-    row_lift<T>(g, L, a.order, higher, a.project, sm, m, wrow, lane);
-    row_store<T>(g, a.g_out + (o + i) * nv, lane, nv);
+    if constexpr (T < 0) {
+      big_row_lift(a.g_out + (o + i) * nv, L, a.order, higher, a.project, m,
+                   sm.wrow + warp * BIG_SCR, lane);
+    } else {
+      double g[Layout<T>::S];
+      row_lift<T>(g, L, a.order, higher, a.project, sm, m, wrow, lane);
+      row_store<T>(g, a.g_out + (o + i) * nv, lane, nv);
+    }
   }
 }
 
@@ -1860,9 +1947,10 @@ __global__ void __launch_bounds__(256) field_kernel(const FieldArgs a) {
 constexpr int kThreads = 256;
 
 static size_t base_smem(int nv, int T, int S, int G, int NT) {
-  size_t s = 128 * 8 + (sizeof(PwPlan) + 15) / 16 * 16 + 4 * (size_t)nv * 8 +
+  size_t s = 128 * 8 + (sizeof(PwPlan) + 15) / 16 * 16 + (T >= 0 ? 4 * (size_t)nv * 8 : 0) +
              2 * (MAX_LEAF + MAX_NODE) * 8 + 64 * 4;
-  if (T == 0) s += (NT / 32) * (size_t)nv * 8;
+  if (T < 0) s += (NT / 32) * (size_t)BIG_SCR * 8;
+  else if (T == 0) s += (NT / 32) * (size_t)nv * 8;
   else if (G < 0) s += (size_t)S * (nv + 8) * 8;
   else s += (size_t)(NT / 32) * S * (G != 0 ? nv + 8 : nv) * 8;
   return s;
@@ -1925,7 +2013,8 @@ static cudaError_t launch_T(const FineArgs& a, int C, cudaStream_t st) {
 
 template <int T>
 static cudaError_t launch_lift_T(const LiftArgs& a, cudaStream_t st) {
-  const size_t smem = 4 * a.m.nv * 8 + (kThreads / 32) * a.m.nv * 8;
+  const size_t smem = T < 0 ? (kThreads / 32) * (size_t)BIG_SCR * 8
+                            : 4 * a.m.nv * 8 + (kThreads / 32) * a.m.nv * 8;
   cudaError_t e =
       cudaFuncSetAttribute(lift_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1934,7 +2023,7 @@ static cudaError_t launch_lift_T(const LiftArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_lift(const LiftArgs& a, cudaStream_t st) {
-  if (a.m.nvyz > 1) return a.m.nv <= 32 * GT ? launch_lift_T<0>(a, st) : cudaErrorInvalidValue;
+  if (a.m.nvyz > 1) return a.m.nv <= 32 * GT ? launch_lift_T<0>(a, st) : launch_lift_T<-1>(a, st);
   switch (a.m.nv) {
     case 64: return launch_lift_T<2>(a, st);
     case 128: return launch_lift_T<4>(a, st);
@@ -1957,9 +2046,9 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
-  if (a.m.nvyz > 1) {  // 1D-3V rows: the generic layout (fast layouts assume one xi axis)
+  if (a.m.nvyz > 1) {  // 1D-3V rows: generic layout up to 256 nodes, big rows beyond
     if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
-    return cudaErrorInvalidValue;
+    return launch_T<-1, 1, 0, 256>(a, C, st);
   }
   switch (a.m.nv) {
     // producer/consumer GS pipeline: 7 consumer warps + 1 producer warp

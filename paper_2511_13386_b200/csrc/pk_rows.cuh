@@ -362,39 +362,48 @@ __device__ __forceinline__ void gen_moments(const double (&g)[GT], const Smem& s
   bsq = gen_bracket(r, wrow, lane, nv, S, dv3);
 }
 
-// Layout dispatch: T == 0 selects the generic layout.
+// Layout dispatch: T == 0 selects the generic layout, T < 0 the big-row
+// layout (pk_big.cuh: the row stays in global memory; callers branch on it).
 template <int T>
 struct Layout {
-  static constexpr int S = T == 0 ? GT : T;
+  static constexpr int S = T == 0 ? GT : (T < 0 ? 1 : T);
 };
 
 template <int T>
 __device__ __forceinline__ void row_load(double (&v)[Layout<T>::S], const double* row, int lane,
                                          int nv) {
-  if constexpr (T == 0) gen_load(v, row, lane, nv);
+  if constexpr (T < 0) return;  // big rows: the callers work on global rows (pk_big.cuh)
+  else if constexpr (T == 0) gen_load(v, row, lane, nv);
   else fast_load<T>(v, row, lane);
 }
 
 template <int T>
 __device__ __forceinline__ void row_store(const double (&v)[Layout<T>::S], double* row, int lane,
                                           int nv) {
-  if constexpr (T == 0) gen_store(v, row, lane, nv);
+  if constexpr (T < 0) return;
+  else if constexpr (T == 0) gen_store(v, row, lane, nv);
   else fast_store<T>(v, row, lane);
 }
 
 template <int T>
 __device__ __forceinline__ void row_zero_store(double* row, int lane, int nv) {
-  double z[Layout<T>::S];
+  if constexpr (T < 0) {
+    for (int c = lane; c < nv; c += 32) __stcg(row + c, 0.0);
+    __syncwarp();
+  } else {
+    double z[Layout<T>::S];
 #pragma unroll
-  for (int s = 0; s < Layout<T>::S; ++s) z[s] = 0.0;
-  row_store<T>(z, row, lane, nv);
+    for (int s = 0; s < Layout<T>::S; ++s) z[s] = 0.0;
+    row_store<T>(z, row, lane, nv);
+  }
 }
 
 template <int T>
 __device__ __forceinline__ void row_moments(const double (&g)[Layout<T>::S], const Smem& sm,
                                             const MeshDev& m, double* wrow, int lane, double& bx,
                                             double& bsq) {
-  if constexpr (T == 0) gen_moments(g, sm, m.nv, m.nvyz, m.dv3, wrow, lane, bx, bsq);
+  if constexpr (T < 0) return;
+  else if constexpr (T == 0) gen_moments(g, sm, m.nv, m.nvyz, m.dv3, wrow, lane, bx, bsq);
   else fast_moments<T>(g, sm, m.dv3, lane, bx, bsq);
 }
 
@@ -402,7 +411,8 @@ template <int T>
 __device__ __forceinline__ void row_lift(double (&g)[Layout<T>::S], const LiftRow& L, int order,
                                          int higher, int project, const Smem& sm,
                                          const MeshDev& m, double* wrow, int lane) {
-  if constexpr (T == 0) gen_lift_row(g, L, order, higher, project, sm, m, wrow, lane);
+  if constexpr (T < 0) return;
+  else if constexpr (T == 0) gen_lift_row(g, L, order, higher, project, sm, m, wrow, lane);
   else fast_lift_row<T>(g, L, order, higher, project, sm, m, lane);
 }
 

@@ -29,8 +29,12 @@ from parakin.poisson import solve_field  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
-# (nx, nvx, nvy, nvz): even / odd nvx, a non-power-of-two nvy*nvz, the 256-node limit
-MESHES = [(16, 8, 4, 4), (12, 7, 4, 4), (10, 6, 5, 4), (16, 16, 4, 4)]
+# (nx, nvx, nvy, nvz): rows of one warp's registers (<= 256 nodes: even / odd
+# nvx, a non-power-of-two nvy*nvz, the 256-node limit) and big rows (the
+# reference's own test/default grid 32x32x16x16, odd nvx with a multi-leaf fold,
+# a folded length whose pairwise split is not a power of two)
+MESHES = [(16, 8, 4, 4), (12, 7, 4, 4), (10, 6, 5, 4), (16, 16, 4, 4),
+          (32, 32, 16, 16), (16, 17, 8, 8), (12, 30, 8, 4)]
 
 
 def digest(a) -> str:
@@ -62,7 +66,8 @@ def main():
         out["M_" + k] = g.M.reshape(-1)
         out["s_" + k] = np.array([m.dx, g.dvx, g.dv3, g.m0, g.m2])
         rho, g0, rb = initial(m)
-        out["in_" + k] = np.concatenate([rho, g0.reshape(-1), [rb]])
+        out["in_" + k] = np.concatenate([rho, [rb]])
+        out["g0_" + k] = np.array(digest(g0))
         E0 = solve_field(rho, rb, m)
         for eps in (0.5, 1e-4):
             p = KineticStepParams.default(m, eps, e_max=float(np.abs(E0).max()))
