@@ -27,6 +27,7 @@ reference's ``_jump_task`` does.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import os
 import time
@@ -35,6 +36,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .adaptation import Thresholds
+from . import _native
 from .engine import Device, make_phase
 from .errors import NonFiniteState
 from .fluid import FluidStepParams, fluid_propagate, substep_sizes
@@ -411,6 +413,7 @@ class _Overlap:
             old = cls._cache.pop(next(iter(cls._cache)))
             old.sync()
         ov.sync()
+        ov.clear_status()
         ov.eng = eng
         ov.Rn = eng.torch.empty_like(eng.row)
         ov.Gn = eng.torch.empty_like(eng.G)
@@ -591,6 +594,14 @@ class _Overlap:
             self.sweep_timeline = [(n, start.elapsed_time(self.ev_fstart[0][n]),
                                     start.elapsed_time(self.ev_row[n])) for n in range(1, ng + 1)]
             self.sweep_wait_s = time.perf_counter() - t_host
+
+    def clear_status(self):
+        """Drop status records latched by speculative work that was never
+        consumed (an iteration that did not happen), before the contexts are
+        reused by another run."""
+        st = _native.PkStatus()
+        for d in [self.cdev] + [d for pair in self.devs[1:] for d in pair]:
+            d._rc(d.lib.pk_status_read(d.ctx, C.byref(st), 1), "status")
 
     def sync(self):
         for pair in self.fs[1:]:
