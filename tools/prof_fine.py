@@ -8,7 +8,6 @@ Prints per-launch CUDA-event times; meant to be wrapped by ncu (-k regex:fine_ke
 import argparse
 import os
 import sys
-import time
 
 import numpy as np
 

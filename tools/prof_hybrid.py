@@ -8,7 +8,6 @@ B copies of a lifted restart state (what parareal windows n >= 2 run).
 import argparse
 import os
 import sys
-import time
 
 import numpy as np
 

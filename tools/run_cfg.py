@@ -63,7 +63,7 @@ def cfg4(args):
 
     import paper_2511_13386_b200 as pk
     from paper_2511_13386_b200 import configs
-    from paper_2511_13386_b200.engine import Device, make_phase
+    from paper_2511_13386_b200.engine import Device
 
     c = configs.cfg4()
     m = c.mesh
