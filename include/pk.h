@@ -104,6 +104,10 @@ int32_t pk_version(void);
  * array of 6 int64 [micro, barrier, slice finish, slice prepare, barrier,
  * steps]; NULL disables. */
 int32_t pk_debug_profile(pk_ctx* ctx, void* dev_counters);
+/* diagnostics: how the calling thread's last pk_fine_propagate launch was
+ * laid out: out[0] CTAs per thread-block cluster, out[1] slices per cluster,
+ * out[2] 1 when the slice vectors were kept in shared memory, out[3] 0. */
+int32_t pk_fine_last_launch(pk_ctx* ctx, int32_t out[4]);
 
 /* --- fine propagator F --------------------------------------------------
  * B independent slices, each advanced through phases[0] then phases[1]

@@ -13,6 +13,7 @@
 
 namespace pk {
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st);
+void fine_last_launch(int out[4]);
 cudaError_t launch_lift(const LiftArgs& a, cudaStream_t st);
 cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
 cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st);
@@ -178,6 +179,14 @@ int32_t pk_version(void) { return 1; }
 int32_t pk_debug_profile(pk_ctx* c, void* dev_counters) {
   if (!c) return PK_ERR_BAD_ARG;
   c->prof = reinterpret_cast<long long*>(dev_counters);
+  return PK_OK;
+}
+
+int32_t pk_fine_last_launch(pk_ctx* c, int32_t out[4]) {
+  if (!c || !out) return PK_ERR_BAD_ARG;
+  int v[4];
+  pk::fine_last_launch(v);
+  for (int i = 0; i < 4; ++i) out[i] = v[i];
   return PK_OK;
 }
 
@@ -351,6 +360,7 @@ int32_t pk_fine_propagate(pk_ctx* c, int32_t B, double* rho, double* E, double* 
     while (C < 8 && B * C * 2 <= slots && c->m.nx >= (C * 2) * 8 * 4) C *= 2;
   }
   a.nwarp_total = C * 8;
+  a.kps = cluster_hint > 0 ? 1 : 0;  // 0: the launcher may pack slices per cluster
   cudaError_t e = pk::launch_fine(a, C, S(stream));
   while (e != cudaSuccess && C > 1) {  // cluster too large for this device: shrink
     cudaGetLastError();

@@ -42,6 +42,7 @@ struct FineArgs {
   MeshDev m;
   int B;
   int nwarp_total;       // warps per slice (cluster CTAs x warps per CTA)
+  int kps;               // slices per cluster (set by the launcher; 1 unless all-kinetic)
   // state
   double* rho;           // [B*nx] in/out
   double* E;             // [B*nx] out: field at the end (also working E)

@@ -22,6 +22,8 @@
 // SURVEY F9).  Arithmetic follows numpy's operation order
 // so results are bitwise equal to the reference.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../include/pk.h"
 #include "pk_rows.cuh"
@@ -133,7 +135,7 @@ __device__ __forceinline__ void bind_shared(SliceView& v, const FineArgs& a, int
 // layout the micro phase writes the row moments straight into the leader's
 // shared memory through DSMEM.
 __device__ __forceinline__ void bind_local(SliceView& v, const FineArgs& a, int b, double* loc,
-                                           bool leader) {
+                                           bool leader, int owner) {
   const int nx = a.m.nx;
   const size_t o = (size_t)b * nx;
   if (loc) {
@@ -157,8 +159,8 @@ __device__ __forceinline__ void bind_local(SliceView& v, const FineArgs& a, int 
     cg::cluster_group cl = cg::this_cluster();
     v.fl = fl;
     v.sq = sq;
-    v.fl_w = cl.map_shared_rank(fl, 0);
-    v.sq_w = a.adaptation ? cl.map_shared_rank(sq, 0) : sq;
+    v.fl_w = cl.map_shared_rank(fl, owner);
+    v.sq_w = a.adaptation ? cl.map_shared_rank(sq, owner) : sq;
     if (!leader) {
       v.rho = v.E = v.Eprev = v.J = v.tA = v.tB = v.tC = v.tD = v.tE = v.bm = v.blift = nullptr;
     }
@@ -1598,6 +1600,39 @@ __device__ bool lift_scalars(const FineArgs& a, const SliceView& v, const Smem& 
   return true;
 }
 
+// Micro phase of a cluster that runs several all-kinetic slices: the
+// cluster's rows, slice after slice, split evenly over its warps; a warp whose
+// share crosses a slice boundary streams each slice's part on its own (row
+// moments go to the owning CTA's shared memory through DSMEM).
+template <int CH, int S>
+__device__ __forceinline__ void micro_slices(const FineArgs& a, const SliceView& v, const Smem& sm,
+                                             int s, int b0, int Kq, int wg, int nwg, double* ring,
+                                             uint64_t* mbar, uint32_t& qbase) {
+  const int nx = a.m.nx, R = Kq * nx;
+  const int r1 = (int)(((long long)(wg + 1) * R) / nwg);
+  for (int r = (int)(((long long)wg * R) / nwg); r < r1;) {
+    const int k = r / nx, bb = b0 + k;
+    const int e = min(r1, (k + 1) * nx);
+    const int n0 = a.ph[0].nsteps[bb], nb = n0 + a.ph[1].nsteps[bb];
+    if (s < nb && !__ldcg(a.abort_ + bb)) {
+      const size_t o = (size_t)bb * nx;
+      SliceView u = v;
+      u.b = bb;
+      u.gJ = a.J + o;
+      u.dco = a.dco + o;
+      u.vco = a.vco + o;
+      u.vsg = a.vsg + o;
+      u.fl_w = cg::this_cluster().map_shared_rank(v.fl, k);
+      double* ga = a.ga + o * a.m.nv;
+      double* gb = a.gb + o * a.m.nv;
+      const bool odd = ((s + (nb & 1)) & 1) != 0;  // step s reads buf(s), as in fine_kernel
+      micro_phase_g8<CH, S, true, false>(a, u, sm, s < n0 ? 0 : 1, odd ? gb : ga, odd ? ga : gb,
+                                         r - k * nx, e - k * nx, ring, mbar, qbase);
+    }
+    r = e;
+  }
+}
+
 __device__ __forceinline__ void cluster_barrier(int C) {
   if (C > 1) {
     cg::this_cluster().sync();
@@ -1624,8 +1659,15 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     C = (int)cl.num_blocks();
     crank = (int)cl.block_rank();
   }
-  const int b = blockIdx.x / C;
-  const bool leader = crank == 0;
+  // a cluster runs K consecutive slices (K = 1 unless the launcher packs
+  // several all-kinetic slices per cluster): CTA k < K owns slice b0 + k (its
+  // slice phase and on-chip vectors), every CTA streams an equal share of the
+  // cluster's rows
+  const int K = a.kps > 1 ? a.kps : 1;
+  const int b0 = (blockIdx.x / C) * K;
+  const int Kq = min(K, a.B - b0);
+  const bool leader = crank < Kq;
+  const int b = leader ? b0 + crank : b0;
   const int nwpc = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   // shared memory carve-up
@@ -1681,9 +1723,12 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
 
   SliceView v;
   bind_shared(v, a, b);
-  bind_local(v, a, b, sm_loc, leader);
+  bind_local(v, a, b, sm_loc, leader, leader ? crank : 0);
   const int n0 = a.ph[0].nsteps[b], n1 = a.ph[1].nsteps[b];
   const int nst = n0 + n1;
+  int nst_all = nst;  // steps of the longest slice of the cluster
+  for (int k = 0; k < Kq && K > 1; ++k)
+    nst_all = max(nst_all, a.ph[0].nsteps[b0 + k] + a.ph[1].nsteps[b0 + k]);
   const int wg = crank * nwpc + warp;
   const int nwg = C * nwpc;
   const int initf = a.init_flags ? a.init_flags[b] : 0;
@@ -1739,27 +1784,34 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     __syncthreads();
   }
   cluster_barrier(C);
-  if (__ldcg(abort_flag)) return;
-  prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, wg, nwg);
+  if (K == 1 && __ldcg(abort_flag)) return;
+  if (K == 1)
+    prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, wg, nwg);
+  else if (leader && !__ldcg(abort_flag))  // several slices: each owner's warps
+    prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, warp, nwpc);
   cluster_barrier(C);
-  if (leader) {
+  if (leader && !__ldcg(abort_flag)) {
     const double dt0 = (n0 > 0 ? a.ph[0].dt : a.ph[1].dt)[b];
     if (!prepare_step<T, AD>(a, v, sm, dt0, 1, buf(0), buf(1), nzf(0), nzf(1), 0)) {
       if (threadIdx.x == 0) *abort_flag = 1;
     }
   }
   cluster_barrier(C);
-  if (__ldcg(abort_flag)) return;
+  if (K == 1 && __ldcg(abort_flag)) return;
 
   // ---- steps ----
   // optional phase profile (slice 0, leader thread 0): clock64 deltas of
   // [micro, barrier, finish, prepare, barrier]
   const bool prof = a.prof && b == 0 && leader && threadIdx.x == 0;
+  // per-CTA [micro, first barrier] cycles and SM id at prof[32 + 3 * blockIdx.x]
+  const bool profc = a.prof && threadIdx.x == 0 && blockIdx.x < 1024;
+  long long pc_m = 0, pc_b = 0, pc_t = 0;
   long long tp[6] = {0, 0, 0, 0, 0, 0};
   long long c0 = prof ? clock64() : 0, c1;
   if (prof) a.prof[6] += c0 - t_kstart;  // prologue
-  for (int s = 0; s < nst; ++s) {
+  for (int s = 0; s < nst_all; ++s) {
     const int ph = s < n0 ? 0 : 1;
+    if (profc) pc_t = clock64();
     if constexpr (G < 0) {
       const int nkk = __ldcg(v.nk);
       const int e0 = (int)(((long long)crank * nkk) / C), e1 = (int)(((long long)(crank + 1) * nkk) / C);
@@ -1768,7 +1820,9 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     } else if constexpr (G > 0) {
       const int nkk = __ldcg(v.nk);
       const int q0 = (int)(((long long)wg * nkk) / nwg), q1 = (int)(((long long)(wg + 1) * nkk) / nwg);
-      if (q0 < q1) {
+      if (!AD && K > 1) {
+        if constexpr (!AD) micro_slices<G, S>(a, v, sm, s, b0, Kq, wg, nwg, ring_w, mbar_w, qbase);
+      } else if (q0 < q1) {
         // the |g|^2 row moment feeds only the adaptation labels
         if constexpr (!AD)
           micro_phase_g8<G, S, true, false>(a, v, sm, ph, buf(s), buf(s + 1), q0, q1, ring_w, mbar_w,
@@ -1788,9 +1842,12 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     else
       micro_phase_big(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     if (prof) { c1 = clock64(); tp[0] += c1 - c0; c0 = c1; }
+    if (profc) { const long long t = clock64(); pc_m += t - pc_t; pc_t = t; }
     cluster_barrier(C);
     if (prof) { c1 = clock64(); tp[1] += c1 - c0; c0 = c1; }
-    if (leader) {
+    if (profc) pc_b += clock64() - pc_t;
+    // (K == 1: s < nst always, and an aborted slice has returned)
+    if (leader && s < nst && !(K > 1 && __ldcg(abort_flag))) {
       bool ok = finish_step(a, v, sm, ph, s);
       if (prof) { c1 = clock64(); tp[2] += c1 - c0; c0 = c1; }
       if (ok && s + 1 < nst) {
@@ -1810,7 +1867,14 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     }
     cluster_barrier(C);
     if (prof) { c1 = clock64(); tp[4] += c1 - c0; c0 = c1; }
-    if (__ldcg(abort_flag)) return;
+    if (K == 1 && __ldcg(abort_flag)) return;
+  }
+  if (profc) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.prof[32 + 3 * blockIdx.x] += pc_m;
+    a.prof[33 + 3 * blockIdx.x] += pc_b;
+    a.prof[34 + 3 * blockIdx.x] = smid;
   }
   if (prof) {
     for (int k = 0; k < 5; ++k) a.prof[k] += tp[k];
@@ -1818,6 +1882,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     a.prof[15] = a.local_smem;
   }
   // ---- epilogue: leader-local state back to the caller's arrays ----
+  if (K > 1 && __ldcg(abort_flag)) return;  // as a single-slice cluster would have
   if (leader && sm_loc) {
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
       a.rho[o + i] = v.rho[i];
@@ -1961,6 +2026,13 @@ static size_t local_smem(int nx, int adaptation) {
                     : (size_t)nx * (NLOC_DK * 8 + NLOC_BK) + 16;
 }
 
+// layout of the calling thread's last fine launch (pk_fine_last_launch)
+static thread_local int last_launch[4] = {0, 0, 0, 0};
+
+void fine_last_launch(int out[4]) {
+  for (int i = 0; i < 4; ++i) out[i] = last_launch[i];
+}
+
 template <int T, int S, int G, int NT, bool AD>
 static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   const size_t base = base_smem(a.m.nv, T, S, G, NT);
@@ -1986,12 +2058,71 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   auto kern = fine_kernel<T, S, G, NT, AD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  static const bool dbg_packing = getenv("PK_DEBUG_PACKING") != nullptr;
+  const bool autok = a.kps == 0;
+  a.kps = 1;
+  if constexpr (!AD && G > 0) {
+    // More slices than SMs (one CTA per slice, some SMs with one CTA and some
+    // with two): pack K slices into clusters of C > K CTAs so that every CTA
+    // streams K/C of a slice, e.g. 200 slices as 67 clusters of 4 CTAs x 3
+    // slices.  Only packings whose clusters are all co-resident (one wave,
+    // cudaOccupancyMaxActiveClusters: GPC packing caps 8-CTA clusters at 33
+    // on a B200, so 256 slices keep one CTA each) qualify.
+    if (autok && C == 1 && a.B > num_sms && a.local_smem && smem <= 112 * 1024) {
+      static size_t q_smem = 0;
+      static int q_max[17];
+      if (q_smem != smem) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        for (int cc = 2; cc <= 16; ++cc) {
+          cudaLaunchConfig_t qc = {};
+          qc.gridDim = dim3(cc);
+          qc.blockDim = dim3(NT);
+          qc.dynamicSmemBytes = smem;
+          cudaLaunchAttribute qa[1];
+          qa[0].id = cudaLaunchAttributeClusterDimension;
+          qa[0].val.clusterDim.x = cc;
+          qa[0].val.clusterDim.y = 1;
+          qa[0].val.clusterDim.z = 1;
+          qc.attrs = qa;
+          qc.numAttrs = 1;
+          int n = 0;
+          if (cudaOccupancyMaxActiveClusters(&n, kern, &qc) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+          }
+          q_max[cc] = n;
+        }
+        q_smem = smem;
+        if (dbg_packing) {
+          fprintf(stderr, "pk packing: smem %zu, max active clusters:", smem);
+          for (int cc = 2; cc <= 16; ++cc) fprintf(stderr, " %d:%d", cc, q_max[cc]);
+          fprintf(stderr, "\n");
+        }
+      }
+      double best = 1.0;
+      for (int cc = 2; cc <= 16; ++cc)
+        for (int kk = 1; kk < cc; ++kk) {
+          const double load = (double)kk / cc;
+          if (load >= best || (a.B + kk - 1) / kk > q_max[cc]) continue;
+          if ((long long)kk * a.m.nx < 32LL * cc * (NT / 32)) continue;  // >= 32 rows per warp
+          best = load;
+          C = cc;
+          a.kps = kk;
+        }
+    }
+  }
+  if (dbg_packing) fprintf(stderr, "pk packing: B %d, cluster of %d CTAs x %d slices\n", a.B, C, a.kps);
+  last_launch[0] = C;
+  last_launch[1] = a.kps;
+  last_launch[2] = a.local_smem;
+  last_launch[3] = 0;
   if (C > 8) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.B * C);
+  cfg.gridDim = dim3((a.B + a.kps - 1) / a.kps * C);
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

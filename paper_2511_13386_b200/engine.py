@@ -222,6 +222,13 @@ class Device:
             msg = self.lib.pk_last_error(self.ctx)
             raise_for(code, f"{what}: {msg.decode() if msg else ''}")
 
+    def last_launch(self):
+        """Layout of this thread's last fine launch: (CTAs per cluster,
+        slices per cluster, slice vectors in shared memory)."""
+        out = (C.c_int32 * 4)()
+        self._rc(self.lib.pk_fine_last_launch(self.ctx, out), "pk_fine_last_launch")
+        return out[0], out[1], bool(out[2])
+
     def check_stream(self, stream):
         """Raise this context's latched status after the work queued on
         `stream` (a torch.cuda.Stream) -- without synchronising the device."""

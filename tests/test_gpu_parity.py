@@ -301,6 +301,59 @@ def test_batched_fine_matches_serial_windows():
         assert eq(g[b].cpu().numpy(), gg)
 
 
+@pytest.mark.parametrize("nv,B", [(64, 170), (128, 200), (128, 180)])
+def test_packed_clusters_match_one_slice_per_cluster(nv, B):
+    """More slices than SMs: the launcher packs K all-kinetic slices into
+    thread-block clusters of C > K CTAs (e.g. 3 slices per 4 CTAs) when all
+    the clusters fit at once.  Step counts differ per slice and one slice
+    trips the solvability guard at entry; every other slice must come out
+    bitwise as with one slice per cluster (cluster_hint=1), and sampled slices
+    equal the oracle."""
+    import torch
+
+    from paper_2511_13386_b200.engine import Device, HybridKnobs, make_phase
+
+    nx, bad = 256, 37
+    cases = configs.cfg5(range(B), nx=nx, nv=nv)
+    m = cases[0].mesh
+    dev = Device.for_mesh(m)
+    grid = O.make_grid(nx, nv)
+    eps = [c.eps for c in cases]
+    dts = [O.stable_dt(grid, c.eps, e_max=float(np.abs(O.field(c.rho, c.rho_bar, grid)).max()))
+           for c in cases]
+    nst = [5 + b % 4 for b in range(B)]
+    rbs = np.array([c.rho_bar for c in cases])
+    rbs[bad] *= 1.01  # inconsistent with the slice's mass: the field guard fails
+    ph = [make_phase(m, eps, dts, nst), make_phase(m, eps, dts, [0] * B)]
+    outs = []
+    for hint in (0, 1):
+        rho = dev.t(np.stack([c.rho for c in cases]))
+        g = dev.t(np.stack([c.g.reshape(nx, nv) for c in cases]))
+        E = torch.zeros_like(rho)
+        Ep = torch.zeros_like(rho)
+        kc = torch.ones((B, nx), dtype=torch.uint8, device=dev.device)
+        ki = torch.ones_like(kc)
+        dev.fine(rho, E, Ep, kc, ki, g, dev.t(rbs), [0] * B, ph, HybridKnobs(), eps, 1e-10,
+                 cluster_hint=hint)
+        with pytest.raises(pk.SolvabilityViolation, match=f"slice {bad},"):
+            dev.check()
+        Cc, K, on_chip = dev.last_launch()
+        assert on_chip
+        if hint == 0:
+            assert 1 < K < Cc, (Cc, K)
+        else:
+            assert (Cc, K) == (1, 1)
+        outs.append([x.cpu().numpy() for x in (rho, E, g)])
+    keep = np.arange(B) != bad
+    for x0, x1 in zip(*outs):
+        assert eq(x0[keep], x1[keep])
+    for b in (0, 6, 7, 8, 100, B - 1):
+        c = cases[b]
+        r, EE, gg = O.kinetic_steps(c.rho, c.g.reshape(nx, nv), nst[b], dts[b], c.eps, grid,
+                                    c.rho_bar)
+        assert eq(outs[0][0][b], r) and eq(outs[0][1][b], EE) and eq(outs[0][2][b], gg)
+
+
 def test_eps_profile_hybrid_vs_oracle():
     """eps(x) extension (cfg3 profile) on a reduced grid: device == oracle restatement."""
     nx, nv = 64, 64

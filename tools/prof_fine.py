@@ -1,6 +1,6 @@
 """Profiling driver for the fine kernel: cfg5-type ensemble, configurable size.
 
-  python tools/prof_fine.py --B 256 --steps 20 [--reps 2] [--nx 1024 --nv 128]
+  python tools/prof_fine.py --B 256 --steps 20 [--reps 2] [--nx 1024 --nv 128] [--per-cta]
 
 Prints per-launch CUDA-event times; meant to be wrapped by ncu (-k regex:fine_kernel).
 """
@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--nx", type=int, default=1024)
     ap.add_argument("--nv", type=int, default=128)
+    ap.add_argument("--per-cta", action="store_true")
     a = ap.parse_args()
     import torch
 
@@ -38,7 +39,7 @@ def main():
     ens = Ensemble(m, [c.eps for c in cases], dts, [c.rho_bar for c in cases])
     rho = torch.from_numpy(np.stack([c.rho for c in cases])).cuda()
     g = torch.from_numpy(np.stack([c.g.reshape(a.nx, a.nv) for c in cases])).cuda()
-    cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(32 + 3 * 1024, dtype=torch.int64, device="cuda")
     ens.dev.lib.pk_debug_profile(ens.dev.ctx, cnt.data_ptr())
     for r in range(a.reps):
         cnt.zero_()
@@ -59,6 +60,25 @@ def main():
         print("   field cycles/step: src %d, pairwise2 %d, corr %d, cumsum %d, mean %d, sub %d"
               % tuple(int(x) // ns for x in c[8:14]))
         print("   slice vectors in shared memory:", bool(c[15]))
+        C, K, _ = ens.dev.last_launch()
+        print(f"   launch: clusters of {C} CTAs x {K} slices")
+        if a.per_cta:
+            ncta = (a.B + K - 1) // K * C
+            pc = c[32:32 + 3 * ncta].reshape(ncta, 3)
+            mic, bar = pc[:, 0] / ns, pc[:, 1] / ns
+            print("   per-CTA micro cycles/step: min %d median %d max %d; first-barrier wait "
+                  "min %d median %d max %d" % (mic.min(), np.median(mic), mic.max(), bar.min(),
+                                               np.median(bar), bar.max()))
+            per_sm = np.bincount(pc[:, 2], minlength=148)
+            for r in range(C):  # by rank within the group
+                sel = np.arange(ncta) % C == r
+                print(f"     rank {r}: micro median {np.median(mic[sel]):.0f}, "
+                      f"SM-mates {np.mean(per_sm[pc[sel, 2]]):.2f}")
+            for nmate in (1, 2):
+                sel = per_sm[pc[:, 2]] == nmate
+                if sel.any():
+                    print(f"     CTAs on SMs holding {nmate}: {sel.sum()}, micro median "
+                          f"{np.median(mic[sel]):.0f}")
 
 
 if __name__ == "__main__":
