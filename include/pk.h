@@ -100,9 +100,10 @@ int32_t pk_status_read(pk_ctx* ctx, pk_status* out, int32_t clear); /* synchroni
    stream, not for the whole device): for contexts driven from several streams. */
 int32_t pk_status_read_stream(pk_ctx* ctx, pk_status* out, int32_t clear, void* stream);
 int32_t pk_version(void);
-/* diagnostics: accumulate per-phase clock64 counters of slice 0 into a device
- * array of 6 int64 [micro, barrier, slice finish, slice prepare, barrier,
- * steps]; NULL disables. */
+/* diagnostics: accumulate clock64 counters into a device array of
+ * 32 + 3 * 1024 int64: [0..5] slice 0's [micro, barrier, slice finish, slice
+ * prepare, barrier, steps], [6..31] slice-phase sub-timers and counts,
+ * [32 + 3c ..] CTA c's [micro, first-barrier wait, SM id]; NULL disables. */
 int32_t pk_debug_profile(pk_ctx* ctx, void* dev_counters);
 /* diagnostics: how the calling thread's last pk_fine_propagate launch was
  * laid out: out[0] CTAs per thread-block cluster, out[1] slices per cluster,

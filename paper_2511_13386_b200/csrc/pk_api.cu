@@ -220,6 +220,16 @@ pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   std::memcpy(h.data() + nv, mesh->M, nv * 8);
   std::memcpy(h.data() + 2 * nv, mesh->xi_M, nv * 8);
   std::memcpy(h.data() + 3 * nv, mesh->w2, nv * 8);
+  m.mirror = 1;
+  for (int j = 0; j < nv; ++j) {
+    const double* vx = h.data();
+    const double* M = h.data() + nv;
+    const double* xM = h.data() + 2 * nv;
+    const double p = vx[j] * M[j];
+    if (vx[nv - 1 - j] != -vx[j] || std::memcmp(&M[nv - 1 - j], &M[j], 8) != 0 ||
+        std::memcmp(&xM[j], &p, 8) != 0)
+      m.mirror = 0;
+  }
   // pairwise plans: x sums (nx terms), and for 1D-3V rows the folded velocity
   // block ((nvx/2) nvy nvz terms) and the middle xi plane (nvy nvz terms)
   PwPlan plan[3];

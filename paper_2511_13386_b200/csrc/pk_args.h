@@ -12,6 +12,8 @@ namespace pk {
 struct MeshDev {
   int nx, nv;
   int nvyz;            // nvy * nvz: stride of the xi axis within a row (1: 1D-x/1D-v)
+  int mirror;          // vx[nv-1-j] == -vx[j], M[nv-1-j] == M[j] and xiM[j] == vx[j]*M[j]
+                       // bit for bit (the reference's mirrored grid, mesh.py:31-44,136)
   double dx, rdx, two_dx, dvx, dv3, m0, m2;
   double three_rb_unused;
   const double* vx;    // [nv] velocity centres xi_j

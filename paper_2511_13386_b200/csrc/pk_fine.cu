@@ -965,7 +965,7 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   const int k = lane & 7, gr = lane >> 3;
   const PhaseDev& P = a.ph[ph];
   const size_t o = (size_t)v.b * nx;
-  const uint32_t s_vx = smem_u32(sm.vx), s_M = smem_u32(sm.M), s_xiM = smem_u32(sm.xiM);
+  const uint32_t s_vx = smem_u32(sm.vx), s_M = smem_u32(sm.M);
   const uint32_t s_ring = smem_u32(ring), s_mbar = smem_u32(mbar);
   const double dx = m.dx, rdx = m.rdx, dv3 = m.dv3;
   const double NaN_ = __longlong_as_double(0x7ff8000000000000LL);
@@ -1131,7 +1131,12 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
 #pragma unroll
       for (int mm = 0; mm < CH; ++mm) {
         const int c = k + 8 * mm, u = NV - 1 - c;
-        const double vxc = lds64(s_vx + 8 * c), vxu = lds64(s_vx + 8 * u);
+        // mirrored grid (m.mirror): vx[u] = -vx[c], M[u] = M[c], and xiM is
+        // vx * M as the host formed it, so one column's constants serve both
+        // halves and xiM costs a multiply instead of a shared-memory load
+        const double vxc = lds64(s_vx + 8 * c), vxu = -vxc;
+        const double Mc = lds64(s_M + 8 * c);
+        const double xMc = vxc * Mc, xMu = -xMc;
         double lo, hi;
         {  // lower half, xi < 0: x-upwind from row i+1; zero inflow at -v*
           const double g = lds64(rcu + 8 * c);
@@ -1140,8 +1145,8 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
           const int cn = up ? c - 1 : c + 1;
           const double nb = cn >= 0 ? lds64(rcu + 8 * cn) : 0.0;
           oo = oo + (g - nb) * svco;
-          oo = oo - lds64(s_M + 8 * c) * dc;
-          const double forcing = oo + lds64(s_xiM + 8 * c) * J;
+          oo = oo - Mc * dc;
+          const double forcing = oo + xMc * J;
           lo = k1 * g - k2 * forcing;
         }
         {  // upper half, xi > 0: x-upwind from row i-1; zero inflow at +v*
@@ -1151,8 +1156,8 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
           const int un = up ? u - 1 : u + 1;
           const double nb = un < NV ? lds64(rcu + 8 * un) : 0.0;
           oo = oo + (g - nb) * svco;
-          oo = oo - lds64(s_M + 8 * u) * dc;
-          const double forcing = oo + lds64(s_xiM + 8 * u) * J;
+          oo = oo - Mc * dc;
+          const double forcing = oo + xMu * J;
           hi = k1 * g - k2 * forcing;
         }
         __stcg(row + c, lo);
@@ -2181,6 +2186,8 @@ cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
     if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
     return launch_T<-1, 1, 0, 256>(a, C, st);
   }
+  if ((a.m.nv == 64 || a.m.nv == 128) && !a.m.mirror)  // G8 needs the mirrored grid
+    return launch_T<0, 1, 0, 256>(a, C, st);
   switch (a.m.nv) {
     // producer/consumer GS pipeline: 7 consumer warps + 1 producer warp
     case 64: return launch_T<2, 16, 4, 128>(a, C, st);   // G8 per-warp rings, 4 warps

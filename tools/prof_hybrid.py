@@ -38,7 +38,7 @@ def main():
     knobs = pk.hybrid.knobs_of(pk.HybridOptions(adaptation=True), pk.Thresholds(1e-3, 1e-3))
     phases = [make_phase(m, [c.eps] * a.B, [kin_p.dt] * a.B, [a.steps] * a.B),
               make_phase(m, [c.eps] * a.B, [kin_p.dt] * a.B, [0] * a.B)]
-    cnt = torch.zeros(32, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(32 + 3 * 1024, dtype=torch.int64, device="cuda")
     dev.lib.pk_debug_profile(dev.ctx, cnt.data_ptr())
     for r in range(a.reps):
         rho = dev.t(np.tile(c.rho, (a.B, 1)))
