@@ -61,6 +61,7 @@ struct FineArgs {
   // hybrid options (hybrid.py:45-55)
   int adaptation, combine_and, reinit, lift_order, time_elim, exact_scan;
   int local_smem;         // leader slice vectors in shared memory (set by the launcher)
+  int scan_smem;          // else: an nx-double field scan buffer in shared memory (launcher)
   double delta0, eta0, rtol;
   const double* rscale;  // [B*nx] eps_c^2 for scale_remainder, or null
   const double* neg_eps; // [B*nx] -eps_i
@@ -73,6 +74,8 @@ struct FineArgs {
   int* kpos;             // [B*nx] row-stream end after each listed row
   int* kstream;          // [B*3nx] row id of each row-stream position
   int* nk;               // [B]
+  int* zlist;            // [B*nx] rows the next micro phase zeroes in its output buffer
+  int* nzl;              // [B] their count
   int* abort_;           // [B]
   Status* status;
   long long* prof;       // [6] optional phase profile (pk_debug_profile), or null

@@ -22,6 +22,7 @@
 // SURVEY F9).  Arithmetic follows numpy's operation order
 // so results are bitwise equal to the reference.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -97,6 +98,8 @@ struct SliceView {
   int* kpos;
   int* kstream;
   int* nk;
+  int* zlist;
+  int* nzl;
   int* abort_;
   double* ga;
   double* gb;
@@ -124,6 +127,8 @@ __device__ __forceinline__ void bind_shared(SliceView& v, const FineArgs& a, int
   v.kpos = a.kpos + o;
   v.kstream = a.kstream + 3 * o;
   v.nk = a.nk + b;
+  v.zlist = a.zlist + o;
+  v.nzl = a.nzl + b;
   v.abort_ = a.abort_ + b;
   v.ga = a.ga + o * a.m.nv;
   v.gb = a.gb + o * a.m.nv;
@@ -288,6 +293,31 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
     dbg[k] += c1 - c0;                     \
     c0 = c1;                               \
   }
+  if (sm.scan && exact_scan && !on_chip) {
+    // global-memory slice vectors with an nx-double buffer on chip: src is
+    // formed where it is read (same bits), the scan and the mean run on the
+    // buffer and E - mean goes straight to E_out
+    double defect, abssum;
+    PK_TICK(0)
+    block_pairwise2([&](int i) { return (rho[i] - rb) * m.dx; }, [&](int i) { return fabs(rho[i]); },
+                    *sm.plan, sm.red, defect, abssum);
+    PK_TICK(1)
+    if (fabs(defect) > rtol * fmax(abssum * m.dx, 2.2250738585072014e-308)) return false;
+    const double corr = defect / (double)nx;
+    double* sc = sm.scan;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) sc[i] = (rho[i] - rb) * m.dx - corr;
+    __syncthreads();
+    PK_TICK(2)
+    smem_cumsum(sc, sc, nx);
+    __syncthreads();
+    PK_TICK(3)
+    const double mean = block_pairwise([&](int i) { return sc[i]; }, *sm.plan, sm.red) / (double)nx;
+    PK_TICK(4)
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) E_out[i] = sc[i] - mean;
+    __syncthreads();
+    PK_TICK(5)
+    return true;
+  }
   for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = (rho[i] - rb) * m.dx;
   __syncthreads();
   PK_TICK(0)
@@ -370,6 +400,56 @@ __device__ __forceinline__ void list_append(bool f, int i, int* list, int* count
   if (f) list[base + __popc(bal & ((1u << lane) - 1u))] = i;
 }
 
+// Who runs a slice phase: the leader CTA alone, or (hybrid slices whose
+// vectors live in global memory) every CTA of the cluster, elements and rows
+// dealt over all of their threads / warps, with cluster barriers between
+// dependent loops and the list counters in the leader's shared memory.
+struct Par {
+  int r0, rs;    // this thread's first element, element stride
+  int w0, ws;    // this warp's first row, row stride
+  int rank, C;   // CTA rank among the participants, participants
+  bool dist;
+  int* flags;    // the leader's misc ints: [0] any flip, [40]/[41] list sizes,
+                 // [42] field ok, [48 + r] scan totals of rank r
+  __device__ void sync() const {
+    if (dist) cg::this_cluster().sync();
+    else __syncthreads();
+  }
+  // exclusive prefix of v over the participants' threads in (rank, thread)
+  // order; returns the total.  `sbuf`: this CTA's block_excl_scan scratch.
+  __device__ int scan(int v, int* pre, int* sbuf) const {
+    int p;
+    const int tot = block_excl_scan(v, &p, sbuf);
+    if (!dist) {
+      *pre = p;
+      return tot;
+    }
+    if (threadIdx.x == 0) flags[48 + rank] = tot;
+    sync();
+    int base = 0, all = 0;
+    for (int r = 0; r < C; ++r) {
+      const int t = flags[48 + r];
+      base += r < rank ? t : 0;
+      all += t;
+    }
+    *pre = p + base;
+    return all;
+  }
+};
+
+__device__ __forceinline__ Par leader_par(const Smem& sm) {
+  Par P;
+  P.r0 = threadIdx.x;
+  P.rs = blockDim.x;
+  P.w0 = threadIdx.x >> 5;
+  P.ws = blockDim.x >> 5;
+  P.rank = 0;
+  P.C = 1;
+  P.dist = false;
+  P.flags = sm.misc;
+  return P;
+}
+
 // ---------------------------------------------------------------------------
 // Slice phase: prepare step `s` (labels, flips, projection coefficients, row
 // list) from rho, E (start of step s), Eprev and the moments fl/sq of the
@@ -377,8 +457,8 @@ __device__ __forceinline__ void list_append(bool f, int i, int* list, int* count
 // (prologue: user g) rather than only on the previous step's kinetic rows.
 template <int T, bool AD>
 __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& sm, double dt,
-                             int moment_all, double* gin, double* gout, uint8_t* nzin,
-                             uint8_t* nzout, int step, long long* dbg = nullptr) {
+                             int moment_all, double* gin, uint8_t* nzin, uint8_t* nzout,
+                             int step, const Par& P, long long* dbg = nullptr) {
   long long c0 = dbg ? clock64() : 0;
 #define PK_PTICK(k)                        \
   if (dbg && threadIdx.x == 0) {           \
@@ -389,8 +469,8 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
-  int* sflags = sm.misc;  // [0]: any flip, [1..32]: scan scratch, [40]/[41]: list sizes
+  const int lane = tid & 31, warp = tid >> 5;
+  int* sflags = P.flags;  // leader's: [0] any flip, [40]/[41] list sizes
 
   if constexpr (!AD) {
     // all-kinetic: J, and the projection/E-upwind coefficients from the
@@ -425,18 +505,18 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   double* __restrict__ tB_ = v.tB;
   {
     constexpr int U = 4;
-    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+    for (int i0 = P.r0; i0 < nx; i0 += U * P.rs) {
       double r0[U], r1[U], e[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = min(i0 + u * nt, nx - 1);
+        const int i = min(i0 + u * P.rs, nx - 1);
         r0[u] = rho_[i];
         r1[u] = rho_[wrap(i + 1, nx)];
         e[u] = E_[i];
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nt;
+        const int i = i0 + u * P.rs;
         if (i < nx) {
           const double J = flux_J(r0[u], r1[u], e[u], m.dx, m.rdx);
           J_[i] = J;
@@ -445,21 +525,21 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       }
     }
   }
-  if (tid == 0) {
+  if (P.rank == 0 && tid == 0) {
     sflags[0] = 0;
     sflags[40] = 0;
     sflags[41] = 0;
   }
-  __syncthreads();
+  P.sync();
   PK_PTICK(0)
   // remainder indicator (adaptation.py:120-152) at cells
   {
     constexpr int U = 4;
-    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+    for (int i0 = P.r0; i0 < nx; i0 += U * P.rs) {
       double e[U], ep[U], j0[U], j1[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = min(i0 + u * nt, nx - 1);
+        const int i = min(i0 + u * P.rs, nx - 1);
         e[u] = E_[i];
         ep[u] = Ep_[i];
         j0[u] = J_[wrap(i - 1, nx)];
@@ -467,7 +547,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nt;
+        const int i = i0 + u * P.rs;
         if (i < nx) {
           tA_[i] = (e[u] - ep[u]) / dt;  // (E - E_prev)/dt
           tB_[i] = 0.5 * (j0[u] + j1[u]);  // J_c
@@ -475,7 +555,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       }
     }
   }
-  __syncthreads();
+  P.sync();
   {
     const double three_rb = 3.0 * v.rb;
     const double* __restrict__ sq_ = v.sq;
@@ -485,12 +565,12 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     uint8_t* __restrict__ kcn_ = v.kcn;
     const double* __restrict__ rsc = a.rscale ? a.rscale + (size_t)v.b * nx : nullptr;
     constexpr int U = 2;
-    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+    for (int i0 = P.r0; i0 < nx; i0 += U * P.rs) {
       double wB[U][7], wR[U][7], a0[U], a1[U], e0[U], e1[U], s0[U], s1[U], rs[U];
       int k0[U], k1[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = min(i0 + u * nt, nx - 1);
+        const int i = min(i0 + u * P.rs, nx - 1);
         const int ip = wrap(i - 1, nx);
 #pragma unroll
         for (int o = 0; o < 7; ++o) {
@@ -510,7 +590,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nt;
+        const int i = i0 + u * P.rs;
         if (i < nx) {
           const double dtEc = 0.5 * (a0[u] + a1[u]);
           const double Ec = 0.5 * (e0[u] + e1[u]);
@@ -537,7 +617,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       }
     }
   }
-  __syncthreads();
+  P.sync();
   PK_PTICK(1)
   // flipped interfaces (F -> K) are listed (klist is free until the row list
   // below), so the row work touches only them
@@ -548,18 +628,18 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     uint8_t* __restrict__ kin_ = v.kin;
     uint8_t* __restrict__ flip_ = v.flip;
     constexpr int U = 4;
-    for (int i00 = 0; i00 < nx; i00 += U * nt) {  // uniform trip count (ballots inside)
+    for (int i00 = 0; i00 < nx; i00 += U * P.rs) {  // uniform trip count (ballots inside)
       int c0[U], c1[U], k[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = min(i00 + u * nt + tid, nx - 1);
+        const int i = min(i00 + u * P.rs + P.r0, nx - 1);
         c0[u] = kcn_[i];
         c1[u] = kcn_[wrap(i + 1, nx)];
         k[u] = ki_[i];
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = i00 + u * nt + tid;
+        const int i = i00 + u * P.rs + P.r0;
         uint8_t f = 0;
         if (i < nx) {
           const uint8_t kin = (uint8_t)(c0[u] | c1[u]);
@@ -573,7 +653,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     }
   }
   if (anyflip) atomicOr(&sflags[0], 1);
-  __syncthreads();
+  P.sync();
   PK_PTICK(2)
   const int nflip = sflags[40];
   if (dbg && tid == 0) dbg[10] += nflip;
@@ -588,15 +668,15 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
         return false;
       }
       // lift scalars at the flipped interfaces (lifting.py:63-88); dE_dt = (E - E_prev)/dt
-      for (int q = tid; q < nflip; q += nt) {
+      for (int q = P.r0; q < nflip; q += P.rs) {
         const int i = v.klist[q];
         const int in_ = wrap(i + 1, nx);
         const double dJ = 0.5 * (v.tD[i] + v.tD[in_]);
         v.tE[i] = dJ - v.E[i] * v.J[i];          // drift
         v.tA[i] = 0.5 * (v.tC[i] + v.tC[in_]);   // R_if
       }
-      __syncthreads();
-      for (int q = warp; q < nflip; q += nwarp) {
+      P.sync();
+      for (int q = P.w0; q < nflip; q += P.ws) {
         const int i = v.klist[q];
         LiftRow L;
         const size_t o = (size_t)v.b * nx + i;
@@ -619,7 +699,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
         if (lane == 0) v.blift[i] = bx;
       }
     } else if (a.reinit == 1) {
-      for (int q = warp; q < nflip; q += nwarp) {
+      for (int q = P.w0; q < nflip; q += P.ws) {
         const int i = v.klist[q];
         row_zero_store<T>(gin + (size_t)i * nv, lane, nv);
         if (lane == 0) v.blift[i] = 0.0;
@@ -629,7 +709,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       return false;
     }
   }
-  __syncthreads();
+  P.sync();
   // masked projection moment (hybrid.py:103-105) on the post-flip rows
   PK_PTICK(3)
   {
@@ -642,12 +722,12 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     const double* __restrict__ fl_ = v.fl;
     double* __restrict__ bm_ = v.bm;
     constexpr int U = 4;
-    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+    for (int i0 = P.r0; i0 < nx; i0 += U * P.rs) {
       int k[U], kn[U], kcv[U], f[U];
       double bl[U], fv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = min(i0 + u * nt, nx - 1);
+        const int i = min(i0 + u * P.rs, nx - 1);
         k[u] = ki_[i];
         kn[u] = kin_[i];
         kcv[u] = kcn_[i];
@@ -657,7 +737,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nt;
+        const int i = i0 + u * P.rs;
         if (i < nx) {
           const bool valid = moment_all || k[u];
           bm_[i] = kn[u] ? (f[u] ? bl[u] : (valid ? fv[u] : 0.0)) : 0.0;
@@ -668,7 +748,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       }
     }
   }
-  __syncthreads();
+  P.sync();
   PK_PTICK(4)
   // projection coefficient dc (kinetic.py:190-191) and E-upwind factor
   // max(E,0)/dvx or min(E,0)/dvx (kinetic.py:177-178); zero the output rows of
@@ -682,12 +762,12 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     int8_t* __restrict__ vsg_ = v.vsg;
     uint8_t* __restrict__ nzo = nzout;
     constexpr int U = 4;
-    for (int i00 = 0; i00 < nx; i00 += U * nt) {  // uniform trip count (ballots inside)
+    for (int i00 = 0; i00 < nx; i00 += U * P.rs) {  // uniform trip count (ballots inside)
       double b1[U], b0[U], e[U];
       int k[U], nz[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = min(i00 + u * nt + tid, nx - 1);
+        const int i = min(i00 + u * P.rs + P.r0, nx - 1);
         b1[u] = bm_[wrap(i + 1, nx)];
         b0[u] = bm_[wrap(i - 1, nx)];
         e[u] = E_[i];
@@ -696,7 +776,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = i00 + u * nt + tid;
+        const int i = i00 + u * P.rs + P.r0;
         bool z = false;
         if (i < nx) {
           dco_[i] = (b1[u] - b0[u]) / m.two_dx;
@@ -705,44 +785,43 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
           z = !k[u] && nz[u];
           if (z) nzo[i] = 0;
         }
-        // rows to zero are listed in kstream (free until the row stream below)
-        list_append(z, i, v.kstream, &sflags[41]);
+        // rows to zero are listed; the next micro phase zeroes them, spread
+        // over every warp of the cluster
+        list_append(z, i, v.zlist, &sflags[41]);
       }
     }
   }
-  __syncthreads();
+  P.sync();
   PK_PTICK(5)
-  {
-    const int nz = sflags[41];
-    if (dbg && tid == 0) dbg[11] += nz;
-    for (int q = warp; q < nz; q += nwarp)
-      row_zero_store<T>(gout + (size_t)v.kstream[q] * nv, lane, nv);
+  if (P.rank == 0 && tid == 0) {
+    *v.nzl = sflags[41];
+    if (dbg) dbg[11] += sflags[41];
   }
-  __syncthreads();
   PK_PTICK(6)
-  // compacted kinetic-row list (order preserving)
-  const int per = (nx + nt - 1) / nt;
-  const int lo = min(nx, tid * per), hi = min(nx, lo + per);
+  // compacted kinetic-row list (order preserving: contiguous chunks per
+  // participating thread, in (rank, thread) order)
+  const int per = (nx + P.rs - 1) / P.rs;
+  const int lo = min(nx, P.r0 * per), hi = min(nx, lo + per);
   int cnt = 0;
   for (int i = lo; i < hi; ++i) cnt += v.ki[i] ? 1 : 0;
   int pre;
-  const int total = block_excl_scan(cnt, &pre, sm.misc + 1);
+  const int total = P.scan(cnt, &pre, sm.misc + 1);
   for (int i = lo; i < hi; ++i)
     if (v.ki[i]) v.klist[pre++] = i;
-  if (tid == 0) *v.nk = total;
+  if (P.rank == 0 && tid == 0) *v.nk = total;
   if (dbg && tid == 0) dbg[12] += total;
-  __syncthreads();
+  P.sync();
   PK_PTICK(7)
   // row-stream positions for the producer/consumer micro phase: entry p needs
   // rows i-1, i, i+1; the rows not already needed by entry p-1 are
   // min(3, i_p - i_{p-1}); kpos[p] = inclusive scan (stream end after p)
   {
-    const int pe = (total + nt - 1) / nt;
-    const int a0 = min(total, tid * pe), a1 = min(total, a0 + pe);
+    const int pe = (total + P.rs - 1) / P.rs;
+    const int a0 = min(total, P.r0 * pe), a1 = min(total, a0 + pe);
     int c = 0;
     for (int q = a0; q < a1; ++q) c += q == 0 ? 3 : min(3, v.klist[q] - v.klist[q - 1]);
     int pre2;
-    block_excl_scan(c, &pre2, sm.misc + 1);
+    P.scan(c, &pre2, sm.misc + 1);
     for (int q = a0; q < a1; ++q) {
       const int i = v.klist[q];
       const int nn = q == 0 ? 3 : min(3, i - v.klist[q - 1]);
@@ -752,7 +831,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       for (int t = 0; t < nn; ++t) v.kstream[pre2 - nn + t] = i + 2 - nn + t;
     }
   }
-  __syncthreads();
+  P.sync();
   PK_PTICK(8)
 #undef PK_PTICK
   return true;
@@ -760,15 +839,16 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
 
 // Slice phase after step s: masked rho update and field.  Returns false on a
 // solvability violation.  kc/ki are the labels the step ran with.
-__device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int ph, int step) {
+__device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int ph, int step,
+                            const Par& Q) {
   const MeshDev& m = a.m;
   const int nx = m.nx;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
   const PhaseDev& P = a.ph[ph];
   const size_t o = (size_t)v.b * nx;
   const double cflu = P.cflu[v.b];
   const double cs = P.cmacs ? P.cmacs[v.b] : __longlong_as_double(0x7ff8000000000000LL);
-  for (int i = tid; i < nx; i += nt) {
+  for (int i = Q.r0; i < nx; i += Q.rs) {
     const int ip = wrap(i - 1, nx);
     const double rho = v.rho[i];
     double r;
@@ -783,15 +863,23 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
     }
     v.rho[i] = r;  // in place: each rho_i update reads only its own rho_i
   }
-  __syncthreads();
+  Q.sync();
   // the new field is solved in place in the E_prev buffer; the old E becomes
   // E_prev (pointer rotation)
   double* t = v.Eprev;
   v.Eprev = v.E;
   v.E = t;
-  if (!slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, a.local_smem != 0, sm,
-                   (a.prof && v.b == 0) ? a.prof + 8 : nullptr)) {
-    if (tid == 0) set_status(a.status, PK_ERR_SOLVABILITY, v.b, step);
+  bool ok = true;
+  if (Q.rank == 0)  // the leader CTA solves the field
+    ok = slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, a.local_smem != 0, sm,
+                     (a.prof && v.b == 0) ? a.prof + 8 : nullptr);
+  if (Q.dist) {
+    if (Q.rank == 0 && tid == 0) Q.flags[42] = ok;
+    Q.sync();
+    ok = Q.flags[42] != 0;
+  }
+  if (!ok) {
+    if (Q.rank == 0 && tid == 0) set_status(a.status, PK_ERR_SOLVABILITY, v.b, step);
     return false;
   }
   return true;
@@ -1652,7 +1740,7 @@ template <int T, int S, int G, int NT, bool AD>
 __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   // ring row stride (doubles); G > 0: per-warp G8 rings, G < 0: CTA-wide
   // producer/consumer ring of the GS layout with SEG = -G
-  constexpr int RSN = G > 0 ? 16 * G + 8 : (G < 0 ? 64 * (-G) + 8 : 32 * T);
+  constexpr int RSN = G > 0 ? 16 * G + 8 : (G < 0 ? 64 * (-G) + 8 : 32 * (T > 0 ? T : 1));
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const long long t_kstart = a.prof ? clock64() : 0;
   const MeshDev& m = a.m;
@@ -1707,7 +1795,8 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       p += (size_t)(G < 0 ? 1 : nwpc) * S * RSN * 8;
     }
     if (a.local_smem) sm_loc = reinterpret_cast<double*>(p);  // same offset in every CTA
-    sm.stage = a.local_smem ? nullptr : reinterpret_cast<double*>(p);
+    sm.stage = a.local_smem || a.scan_smem ? nullptr : reinterpret_cast<double*>(p);
+    sm.scan = !a.local_smem && a.scan_smem ? reinterpret_cast<double*>(p) : nullptr;
     sm.smb = mbar + 120;  // slots past every ring's mbarriers
   }
   {
@@ -1795,9 +1884,23 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   else if (leader && !__ldcg(abort_flag))  // several slices: each owner's warps
     prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, warp, nwpc);
   cluster_barrier(C);
-  if (leader && !__ldcg(abort_flag)) {
+  // hybrid slices with global-memory vectors run their slice phases on every
+  // CTA of the cluster; otherwise the leader runs them alone
+  Par par = leader_par(sm);
+  const bool dist = AD && C > 1 && K == 1 && !sm_loc;
+  if (dist) {
+    par.rank = crank;
+    par.C = C;
+    par.dist = true;
+    par.r0 = crank * blockDim.x + threadIdx.x;
+    par.rs = C * blockDim.x;
+    par.w0 = crank * nwpc + warp;
+    par.ws = C * nwpc;
+    par.flags = cg::this_cluster().map_shared_rank(sm.misc, 0);
+  }
+  if ((dist || leader) && !__ldcg(abort_flag)) {
     const double dt0 = (n0 > 0 ? a.ph[0].dt : a.ph[1].dt)[b];
-    if (!prepare_step<T, AD>(a, v, sm, dt0, 1, buf(0), buf(1), nzf(0), nzf(1), 0)) {
+    if (!prepare_step<T, AD>(a, v, sm, dt0, 1, buf(0), nzf(0), nzf(1), 0, par)) {
       if (threadIdx.x == 0) *abort_flag = 1;
     }
   }
@@ -1816,6 +1919,11 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   if (prof) a.prof[6] += c0 - t_kstart;  // prologue
   for (int s = 0; s < nst_all; ++s) {
     const int ph = s < n0 ? 0 : 1;
+    if constexpr (AD) {  // rows the slice phase listed for zeroing in this step's output
+      const int nzr = __ldcg(v.nzl);
+      for (int q = wg; q < nzr; q += nwg)
+        row_zero_store<T>(buf(s + 1) + (size_t)__ldcg(v.zlist + q) * nv, threadIdx.x & 31, nv);
+    }
     if (profc) pc_t = clock64();
     if constexpr (G < 0) {
       const int nkk = __ldcg(v.nk);
@@ -1852,20 +1960,20 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     if (prof) { c1 = clock64(); tp[1] += c1 - c0; c0 = c1; }
     if (profc) pc_b += clock64() - pc_t;
     // (K == 1: s < nst always, and an aborted slice has returned)
-    if (leader && s < nst && !(K > 1 && __ldcg(abort_flag))) {
-      bool ok = finish_step(a, v, sm, ph, s);
+    if ((dist || leader) && s < nst && !(K > 1 && __ldcg(abort_flag))) {
+      bool ok = finish_step(a, v, sm, ph, s, par);
       if (prof) { c1 = clock64(); tp[2] += c1 - c0; c0 = c1; }
       if (ok && s + 1 < nst) {
         // step s+1 reads buf(s+1) and writes buf(s+2) == buf(s); after step
         // s the rows of buf(s+1) hold data exactly on step s's kinetic rows.
         if (AD) {
           uint8_t* nzn = nzf(s + 1);
-          for (int i = threadIdx.x; i < nx; i += blockDim.x) nzn[i] = v.ki[i];
-          __syncthreads();
+          for (int i = par.r0; i < nx; i += par.rs) nzn[i] = v.ki[i];
+          par.sync();
         }
         const int phn = (s + 1) < n0 ? 0 : 1;
-        ok = prepare_step<T, AD>(a, v, sm, a.ph[phn].dt[b], 0, buf(s + 1), buf(s), nzf(s + 1),
-                             nzf(s), s + 1, (a.prof && b == 0) ? a.prof + 16 : nullptr);
+        ok = prepare_step<T, AD>(a, v, sm, a.ph[phn].dt[b], 0, buf(s + 1), nzf(s + 1), nzf(s),
+                                 s + 1, par, (a.prof && b == 0 && leader) ? a.prof + 16 : nullptr);
       }
       if (!ok && threadIdx.x == 0) *abort_flag = 1;
       if (prof) { c1 = clock64(); tp[3] += c1 - c0; c0 = c1; }
@@ -2056,9 +2164,13 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   const size_t limit = (size_t)a.B * C <= (size_t)num_sms ? 226 * 1024 : 112 * 1024;
   size_t smem = base + STAGE_NS * STAGE_CH * 8;  // scan staging ring
   a.local_smem = 0;
+  a.scan_smem = 0;
   if (base + local_smem(a.m.nx, a.adaptation) <= limit) {
     a.local_smem = 1;
     smem = base + local_smem(a.m.nx, a.adaptation);
+  } else if (base + (size_t)a.m.nx * 8 <= limit) {  // the field scan on chip
+    a.scan_smem = 1;
+    smem = std::max(smem, base + (size_t)a.m.nx * 8);
   }
   auto kern = fine_kernel<T, S, G, NT, AD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

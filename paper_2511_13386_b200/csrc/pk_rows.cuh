@@ -18,6 +18,7 @@ struct Smem {
   double* wrow;   // generic rows: one nv-row per warp
   int* misc;      // small ints
   double* stage = nullptr;  // scan staging ring (global-memory slice vectors), or null
+  double* scan = nullptr;   // [nx] field scan buffer (global-memory slice vectors), or null
   uint64_t* smb = nullptr;  // its mbarriers
 };
 
