@@ -198,41 +198,59 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
-// warp_cumsum for operands that live in shared memory: explicit LDS/STS
-// (generic accesses cost ~2x the chain latency).  dst may alias src: every
-// operand is loaded before its slot is overwritten.  Two register blocks
-// alternate (ping-pong, no register copies): block A's adds run while block
-// B's loads are in flight, so the only serial dependency is the add chain.
+// Eight elements of the smem_cumsum chain in one asm block: the next block's
+// eight operands are loaded first (into n*), then acc += c_k and the running
+// sum is stored, k = 0..7.  One block keeps the compiler from sinking the
+// loads next to their adds, which it does under register pressure (kernels
+// capped at 128 registers) and which doubles the chain's cost.
+#define PK_CS8(acc, c, nn, lda, sta)                                                      \
+  asm volatile(                                                                            \
+      "{\n\t"                                                                              \
+      "ld.shared.f64 %1, [%17];\n\t"                                                       \
+      "ld.shared.f64 %2, [%17+8];\n\t"                                                     \
+      "ld.shared.f64 %3, [%17+16];\n\t"                                                    \
+      "ld.shared.f64 %4, [%17+24];\n\t"                                                    \
+      "ld.shared.f64 %5, [%17+32];\n\t"                                                    \
+      "ld.shared.f64 %6, [%17+40];\n\t"                                                    \
+      "ld.shared.f64 %7, [%17+48];\n\t"                                                    \
+      "ld.shared.f64 %8, [%17+56];\n\t"                                                    \
+      "add.rn.f64 %0, %0, %9;\n\tst.shared.f64 [%18], %0;\n\t"                             \
+      "add.rn.f64 %0, %0, %10;\n\tst.shared.f64 [%18+8], %0;\n\t"                          \
+      "add.rn.f64 %0, %0, %11;\n\tst.shared.f64 [%18+16], %0;\n\t"                         \
+      "add.rn.f64 %0, %0, %12;\n\tst.shared.f64 [%18+24], %0;\n\t"                         \
+      "add.rn.f64 %0, %0, %13;\n\tst.shared.f64 [%18+32], %0;\n\t"                         \
+      "add.rn.f64 %0, %0, %14;\n\tst.shared.f64 [%18+40], %0;\n\t"                         \
+      "add.rn.f64 %0, %0, %15;\n\tst.shared.f64 [%18+48], %0;\n\t"                         \
+      "add.rn.f64 %0, %0, %16;\n\tst.shared.f64 [%18+56], %0;\n\t"                         \
+      "}"                                                                                   \
+      : "+d"(acc), "=&d"(nn[0]), "=&d"(nn[1]), "=&d"(nn[2]), "=&d"(nn[3]), "=&d"(nn[4]),   \
+        "=&d"(nn[5]), "=&d"(nn[6]), "=&d"(nn[7])                                           \
+      : "d"(c[0]), "d"(c[1]), "d"(c[2]), "d"(c[3]), "d"(c[4]), "d"(c[5]), "d"(c[6]),       \
+        "d"(c[7]), "r"(lda), "r"(sta)                                                      \
+      : "memory")
+
+// warp_cumsum for operands that live in shared memory (dst may alias src:
+// every operand is loaded before its slot is overwritten).  Two blocks of
+// eight operands alternate (ping-pong, no register copies): one block's adds
+// run while the other block's loads are in flight, so the only serial
+// dependency is the add chain (~8 cycles per element, tools/cumsum_bench.cu).
 // Keep the operand a plain load: an extra DADD per element (e.g. a fused
-// subtrahend) doubles the cost (tools/cumsum_bench.cu).  Thread 0 only.
+// subtrahend) doubles the cost.  Thread 0 only.
 __device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int n) {
   if (threadIdx.x != 0) return;
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(src);
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-  constexpr int K = 8;
   double acc = -0.0;
-  const int n2 = n - n % (2 * K);
-  double A[K], Bv[K];
+  const int n2 = n - n % 16;
   if (n2 > 0) {
+    double A[8], Bv[8];
 #pragma unroll
-    for (int k = 0; k < K; ++k) A[k] = lds64(s + 8 * k);
-  }
-  for (int i = 0; i < n2; i += 2 * K) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) Bv[k] = lds64(s + 8 * (i + K + k));
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      acc = acc + A[k];
-      sts64(d + 8 * (i + k), acc);
-    }
-    if (i + 2 * K < n2) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) A[k] = lds64(s + 8 * (i + 2 * K + k));
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      acc = acc + Bv[k];
-      sts64(d + 8 * (i + K + k), acc);
+    for (int k = 0; k < 8; ++k) A[k] = lds64(s + 8 * k);
+    for (int i = 0; i < n2; i += 16) {
+      PK_CS8(acc, A, Bv, s + 8 * (i + 8), d + 8 * i);
+      // the last block re-reads the first eight operands (harmless, unused)
+      const uint32_t nxt = i + 16 < n2 ? s + 8 * (i + 16) : s;
+      PK_CS8(acc, Bv, A, nxt, d + 8 * (i + 8));
     }
   }
   for (int i = n2; i < n; ++i) {
