@@ -61,7 +61,7 @@ struct FineArgs {
   // hybrid options (hybrid.py:45-55)
   int adaptation, combine_and, reinit, lift_order, time_elim, exact_scan;
   int local_smem;         // leader slice vectors in shared memory (set by the launcher)
-  int scan_smem;          // else: an nx-double field scan buffer in shared memory (launcher)
+  int scan_smem;          // else: doubles of the field scan buffer in shared memory (launcher)
   double delta0, eta0, rtol;
   const double* rscale;  // [B*nx] eps_c^2 for scale_remainder, or null
   const double* neg_eps; // [B*nx] -eps_i

@@ -235,12 +235,14 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
 // run while the other block's loads are in flight, so the only serial
 // dependency is the add chain (~8 cycles per element, tools/cumsum_bench.cu).
 // Keep the operand a plain load: an extra DADD per element (e.g. a fused
-// subtrahend) doubles the cost.  Thread 0 only.
-__device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int n) {
+// subtrahend) doubles the cost.  Thread 0 only.  `init`: the chain's carry
+// (-0.0 starts np.cumsum: -0 + x == x for every x).
+__device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int n,
+                                            double init = -0.0) {
   if (threadIdx.x != 0) return;
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(src);
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-  double acc = -0.0;
+  double acc = init;
   const int n2 = n - n % 16;
   if (n2 > 0) {
     double A[8], Bv[8];

@@ -219,66 +219,6 @@ __device__ __forceinline__ double stencil_reg(const double (&w)[7], const MeshDe
   return acc * m.sts[p - 1];
 }
 
-// np.cumsum of a global-memory vector staged through shared memory: thread 0
-// streams 2 KB chunks with TMA bulk copies (4-slot ring, three chunks ahead,
-// so the L2 latency hides behind the add chain) and runs the ping-pong LDS
-// chain over each chunk; results go to dst with plain stores.  dst may alias
-// src: chunk c+4 is fetched after elements < (c+1)*256 are written.  n even
-// (bulk copies move 16-byte granules).  Thread 0 only.
-constexpr int STAGE_CH = 256, STAGE_NS = 4;
-
-__device__ void staged_cumsum(const double* src, double* dst, int n, double* stage, uint64_t* mb) {
-  if (threadIdx.x != 0) return;
-  const int nch = (n + STAGE_CH - 1) / STAGE_CH;
-  for (int s = 0; s < STAGE_NS; ++s) mbar_init(mb + s, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  fence_proxy_async_global();  // src was written by the generic proxy
-  auto issue = [&](int c) {
-    const uint32_t bytes = (uint32_t)min(STAGE_CH, n - c * STAGE_CH) * 8u;
-    uint64_t* m = mb + c % STAGE_NS;
-    mbar_expect_tx(m, bytes);
-    bulk_g2s(stage + (c % STAGE_NS) * STAGE_CH, src + (size_t)c * STAGE_CH, bytes, m);
-  };
-  for (int c = 0; c < min(STAGE_NS, nch); ++c) issue(c);
-  double acc = -0.0;
-  for (int c = 0; c < nch; ++c) {
-    mbar_wait(mb + c % STAGE_NS, (uint32_t)(c / STAGE_NS) & 1u);
-    const uint32_t s0 = smem_u32(stage + (c % STAGE_NS) * STAGE_CH);
-    double* d = dst + (size_t)c * STAGE_CH;
-    const int len = min(STAGE_CH, n - c * STAGE_CH);
-    constexpr int K = 8;
-    const int n2 = len - len % (2 * K);
-    double A[K], Bv[K];
-    if (n2 > 0) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) A[k] = lds64(s0 + 8 * k);
-    }
-    for (int i = 0; i < n2; i += 2 * K) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) Bv[k] = lds64(s0 + 8 * (i + K + k));
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        acc = acc + A[k];
-        d[i + k] = acc;
-      }
-      if (i + 2 * K < n2) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) A[k] = lds64(s0 + 8 * (i + 2 * K + k));
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        acc = acc + Bv[k];
-        d[i + K + k] = acc;
-      }
-    }
-    for (int i = n2; i < len; ++i) {
-      acc = acc + lds64(s0 + 8 * i);
-      d[i] = acc;
-    }
-    if (c + STAGE_NS < nch) issue(c + STAGE_NS);  // slot consumed (values in registers)
-  }
-}
-
 // E_out = solve_field(rho); false on a solvability violation.
 // poisson.py:41-54: src=(rho-rb)dx; defect=sum(src); guard; src-=defect/nx;
 // E=cumsum(src); E-=mean(E).
@@ -294,9 +234,9 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
     c0 = c1;                               \
   }
   if (sm.scan && exact_scan && !on_chip) {
-    // global-memory slice vectors with an nx-double buffer on chip: src is
-    // formed where it is read (same bits), the scan and the mean run on the
-    // buffer and E - mean goes straight to E_out
+    // global-memory slice vectors with a buffer of scan_cap doubles on chip:
+    // src is formed where it is read (same bits), the scan runs on the buffer
+    // (chunk by chunk, the carry continuing the chain, when nx > scan_cap)
     double defect, abssum;
     PK_TICK(0)
     block_pairwise2([&](int i) { return (rho[i] - rb) * m.dx; }, [&](int i) { return fabs(rho[i]); },
@@ -305,15 +245,38 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
     if (fabs(defect) > rtol * fmax(abssum * m.dx, 2.2250738585072014e-308)) return false;
     const double corr = defect / (double)nx;
     double* sc = sm.scan;
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) sc[i] = (rho[i] - rb) * m.dx - corr;
-    __syncthreads();
-    PK_TICK(2)
-    smem_cumsum(sc, sc, nx);
-    __syncthreads();
+    if (sm.scan_cap >= nx) {  // whole: the mean and E - mean from the buffer too
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) sc[i] = (rho[i] - rb) * m.dx - corr;
+      __syncthreads();
+      PK_TICK(2)
+      smem_cumsum(sc, sc, nx, -0.0);
+      __syncthreads();
+      PK_TICK(3)
+      const double mean =
+          block_pairwise([&](int i) { return sc[i]; }, *sm.plan, sm.red) / (double)nx;
+      PK_TICK(4)
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) E_out[i] = sc[i] - mean;
+      __syncthreads();
+      PK_TICK(5)
+      return true;
+    }
+    double carry = -0.0;  // np.cumsum's chain starts from the first operand
+    for (int c0 = 0; c0 < nx; c0 += sm.scan_cap) {
+      const int len = min(sm.scan_cap, nx - c0);
+      for (int i = threadIdx.x; i < len; i += blockDim.x)
+        sc[i] = (rho[c0 + i] - rb) * m.dx - corr;
+      __syncthreads();
+      smem_cumsum(sc, sc, len, carry);
+      __syncthreads();
+      carry = sc[len - 1];
+      for (int i = threadIdx.x; i < len; i += blockDim.x) E_out[c0 + i] = sc[i];
+      __syncthreads();
+    }
     PK_TICK(3)
-    const double mean = block_pairwise([&](int i) { return sc[i]; }, *sm.plan, sm.red) / (double)nx;
+    const double mean =
+        block_pairwise([&](int i) { return E_out[i]; }, *sm.plan, sm.red) / (double)nx;
     PK_TICK(4)
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) E_out[i] = sc[i] - mean;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) E_out[i] = E_out[i] - mean;
     __syncthreads();
     PK_TICK(5)
     return true;
@@ -336,8 +299,6 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
   if (exact_scan) {
     if (on_chip)  // src and E_out in this CTA's shared memory
       smem_cumsum(src, E_out, nx);
-    else if (sm.stage && nx % 2 == 0)
-      staged_cumsum(src, E_out, nx, sm.stage, sm.smb);
     else
       warp_cumsum([&](int i) { return src[i]; }, [&](int i, double v) { E_out[i] = v; }, nx);
   } else {
@@ -1795,9 +1756,8 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       p += (size_t)(G < 0 ? 1 : nwpc) * S * RSN * 8;
     }
     if (a.local_smem) sm_loc = reinterpret_cast<double*>(p);  // same offset in every CTA
-    sm.stage = a.local_smem || a.scan_smem ? nullptr : reinterpret_cast<double*>(p);
     sm.scan = !a.local_smem && a.scan_smem ? reinterpret_cast<double*>(p) : nullptr;
-    sm.smb = mbar + 120;  // slots past every ring's mbarriers
+    sm.scan_cap = a.scan_smem;
   }
   {
     const int* src = reinterpret_cast<const int*>(m.plan_x);
@@ -2162,15 +2122,24 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   if (need > 112 * 1024 && need <= 226 * 1024 && C >= 2 && (size_t)a.B * (C / 2) <= (size_t)num_sms)
     C /= 2;
   const size_t limit = (size_t)a.B * C <= (size_t)num_sms ? 226 * 1024 : 112 * 1024;
-  size_t smem = base + STAGE_NS * STAGE_CH * 8;  // scan staging ring
+  // test hook: PK_FORCE_GLOBAL_SLICE=1 keeps the slice vectors in global
+  // memory (whole scan buffer on chip), =2 also cuts the scan buffer to 48
+  // doubles (chunked scan), so small golden cases exercise the large-nx paths
+  static const int force_global =
+      getenv("PK_FORCE_GLOBAL_SLICE") ? atoi(getenv("PK_FORCE_GLOBAL_SLICE")) : 0;
+  size_t smem;
   a.local_smem = 0;
   a.scan_smem = 0;
-  if (base + local_smem(a.m.nx, a.adaptation) <= limit) {
+  if (!force_global && base + local_smem(a.m.nx, a.adaptation) <= limit) {
     a.local_smem = 1;
     smem = base + local_smem(a.m.nx, a.adaptation);
-  } else if (base + (size_t)a.m.nx * 8 <= limit) {  // the field scan on chip
-    a.scan_smem = 1;
-    smem = std::max(smem, base + (size_t)a.m.nx * 8);
+  } else {  // global slice vectors, the field scan through an on-chip buffer
+    const size_t room = limit > base ? (limit - base) / 8 : 0;
+    int cap = (int)std::min<size_t>((size_t)a.m.nx, room);
+    if (force_global == 2) cap = std::min(cap, 48);
+    if (cap < std::min(16, a.m.nx)) return cudaErrorInvalidValue;  // (never: tens of KB left)
+    a.scan_smem = cap;
+    smem = base + (size_t)cap * 8;
   }
   auto kern = fine_kernel<T, S, G, NT, AD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

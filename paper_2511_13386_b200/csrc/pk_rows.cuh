@@ -17,9 +17,8 @@ struct Smem {
   double* red;    // pairwise scratch (MAX_LEAF + MAX_NODE)
   double* wrow;   // generic rows: one nv-row per warp
   int* misc;      // small ints
-  double* stage = nullptr;  // scan staging ring (global-memory slice vectors), or null
-  double* scan = nullptr;   // [nx] field scan buffer (global-memory slice vectors), or null
-  uint64_t* smb = nullptr;  // its mbarriers
+  double* scan = nullptr;   // field scan buffer (global-memory slice vectors), or null
+  int scan_cap = 0;         // its capacity in doubles (chunks of it when < nx)
 };
 
 // ---------------------------------------------------------------------------
