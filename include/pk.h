@@ -106,8 +106,10 @@ int32_t pk_version(void);
  * [32 + 3c ..] CTA c's [micro, first-barrier wait, SM id]; NULL disables. */
 int32_t pk_debug_profile(pk_ctx* ctx, void* dev_counters);
 /* diagnostics: how the calling thread's last pk_fine_propagate launch was
- * laid out: out[0] CTAs per thread-block cluster, out[1] slices per cluster,
- * out[2] 1 when the slice vectors were kept in shared memory, out[3] 0. */
+ * laid out: out[0] CTAs per thread-block cluster (or software group), out[1]
+ * slices per cluster, out[2] 1 when the slice vectors were kept in shared
+ * memory, out[3] 1 when the group was a software group (cooperative launch,
+ * moments through global memory) rather than a hardware cluster. */
 int32_t pk_fine_last_launch(pk_ctx* ctx, int32_t out[4]);
 
 /* --- fine propagator F --------------------------------------------------

@@ -138,8 +138,8 @@ int ensure(pk_ctx* c, int B) {
   if ((e = cudaMalloc(&c->dws, NDWS * n * sizeof(double))) != cudaSuccess) return cuda_fail(c, e, "workspace");
   if ((e = cudaMalloc(&c->i8ws, n)) != cudaSuccess) return cuda_fail(c, e, "workspace");
   if ((e = cudaMalloc(&c->u8ws, NU8 * n)) != cudaSuccess) return cuda_fail(c, e, "workspace");
-  // klist [n], nk [B], abort [B], kpos [n], kstream [3n], zlist [n], nzl [B]
-  if ((e = cudaMalloc(&c->iws, (6 * n + 3 * (size_t)B) * sizeof(int))) != cudaSuccess)
+  // klist [n], nk [B], abort [B], kpos [n], kstream [3n], zlist [n], nzl [B], sg_cnt [B]
+  if ((e = cudaMalloc(&c->iws, (6 * n + 4 * (size_t)B) * sizeof(int))) != cudaSuccess)
     return cuda_fail(c, e, "workspace");
   c->cap = B;
   return PK_OK;
@@ -166,6 +166,7 @@ void bind_ws(pk_ctx* c, pk::FineArgs& a) {
   a.kstream = a.kpos + n;
   a.zlist = a.kstream + 3 * n;
   a.nzl = a.zlist + n;
+  a.sg_cnt = reinterpret_cast<unsigned*>(a.nzl + c->cap);
   a.status = c->d_status;
   a.prof = c->prof;
 }

@@ -45,6 +45,9 @@ struct FineArgs {
   int B;
   int nwarp_total;       // warps per slice (cluster CTAs x warps per CTA)
   int kps;               // slices per cluster (set by the launcher; 1 unless all-kinetic)
+  int sg;                // > 1: the "cluster" is a software group of sg CTAs (no hardware
+                         // cluster; moments through global memory, barriers on sg_cnt)
+  unsigned* sg_cnt;      // [B] per-group arrival counters (zeroed by the launcher)
   // state
   double* rho;           // [B*nx] in/out
   double* E;             // [B*nx] out: field at the end (also working E)

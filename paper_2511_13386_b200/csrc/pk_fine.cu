@@ -1676,7 +1676,7 @@ __device__ __forceinline__ void micro_slices(const FineArgs& a, const SliceView&
       u.dco = a.dco + o;
       u.vco = a.vco + o;
       u.vsg = a.vsg + o;
-      u.fl_w = cg::this_cluster().map_shared_rank(v.fl, k);
+      u.fl_w = a.sg > 1 ? a.fl + o : cg::this_cluster().map_shared_rank(v.fl, k);
       double* ga = a.ga + o * a.m.nv;
       double* gb = a.gb + o * a.m.nv;
       const bool odd = ((s + (nb & 1)) & 1) != 0;  // step s reads buf(s), as in fine_kernel
@@ -1695,6 +1695,38 @@ __device__ __forceinline__ void cluster_barrier(int C) {
   }
 }
 
+// Barrier of a software group (FineArgs::sg): C co-resident CTAs (cooperative
+// launch) count arrivals on one global counter; the n-th barrier of the
+// kernel waits for C * n arrivals.  Release/acquire at gpu scope, as a grid
+// sync: every write before the barrier is visible to every CTA after it.
+constexpr unsigned long long kMomentSentinel = 0x7FF4C0DE5E47C0DEull;  // signalling NaN
+
+__device__ __forceinline__ void st_relaxed_u64(double* p, unsigned long long x) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+  unsigned long long x;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+  return x;
+}
+
+__device__ __forceinline__ void group_barrier(unsigned* cnt, int C, unsigned& n) {
+  __syncthreads();
+  ++n;
+  if (threadIdx.x == 0) {
+    const unsigned target = (unsigned)C * n;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
 // AD: adaptation on (hybrid) or off (all-kinetic, compiled without the
 // labels / lifts / row lists of the hybrid slice phase)
 template <int T, int S, int G, int NT, bool AD>
@@ -1708,11 +1740,20 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   const int nx = m.nx, nv = m.nv;
   int C = 1;
   int crank = 0;
-  {
+  if (a.sg > 1) {  // software group of sg consecutive CTAs (hardware cluster of 1)
+    C = a.sg;
+    crank = (int)(blockIdx.x % (unsigned)C);
+  } else {
     cg::cluster_group cl = cg::this_cluster();
     C = (int)cl.num_blocks();
     crank = (int)cl.block_rank();
   }
+  unsigned* const sgc = a.sg > 1 ? a.sg_cnt + blockIdx.x / (unsigned)C : nullptr;
+  unsigned sgn = 0;
+  auto barrier = [&]() {
+    if (sgc) group_barrier(sgc, C, sgn);
+    else cluster_barrier(C);
+  };
   // a cluster runs K consecutive slices (K = 1 unless the launcher packs
   // several all-kinetic slices per cluster): CTA k < K owns slice b0 + k (its
   // slice phase and on-chip vectors), every CTA streams an equal share of the
@@ -1778,6 +1819,46 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
   SliceView v;
   bind_shared(v, a, b);
   bind_local(v, a, b, sm_loc, leader, leader ? crank : 0);
+  // Software group: the row moments arrive in global memory (a.fl), the value
+  // being its own flag -- the owner re-arms every entry with a signalling-NaN
+  // sentinel (arithmetic only makes quiet NaNs) before the barrier that opens
+  // the next micro phase, and after that phase polls its entries until none
+  // is the sentinel, pulling them on chip.  No barrier (and no release fence
+  // behind the phase's row stores) between the micro and the slice phase.
+  const bool sgo = a.sg > 1 && leader && sm_loc;  // an owner in a software group
+  if (a.sg > 1) v.fl_w = a.fl + (size_t)b * nx;
+  auto arm_moments = [&]() {
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) st_relaxed_u64(v.fl_w + i, kMomentSentinel);
+  };
+  auto pull_moments = [&]() {  // moments written by this CTA (prologue)
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) v.fl[i] = __ldcg(v.fl_w + i);
+    __syncthreads();
+    arm_moments();
+  };
+  auto poll_moments = [&]() {  // moments written by the whole group (micro phase)
+    constexpr int U = 8;
+    for (int i0 = threadIdx.x; i0 < nx; i0 += U * blockDim.x) {
+      unsigned long long x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        x[u] = i < nx ? ld_relaxed_u64(v.fl_w + i) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < nx) {
+          while (x[u] == kMomentSentinel) {
+            __nanosleep(64);
+            x[u] = ld_relaxed_u64(v.fl_w + i);
+          }
+          v.fl[i] = __longlong_as_double((long long)x[u]);
+        }
+      }
+    }
+    __syncthreads();
+    arm_moments();
+  };
   const int n0 = a.ph[0].nsteps[b], n1 = a.ph[1].nsteps[b];
   const int nst = n0 + n1;
   int nst_all = nst;  // steps of the longest slice of the cluster
@@ -1837,13 +1918,14 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     }
     __syncthreads();
   }
-  cluster_barrier(C);
+  barrier();
   if (K == 1 && __ldcg(abort_flag)) return;
   if (K == 1)
     prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, wg, nwg);
   else if (leader && !__ldcg(abort_flag))  // several slices: each owner's warps
     prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, warp, nwpc);
-  cluster_barrier(C);
+  barrier();
+  if (sgo) pull_moments();
   // hybrid slices with global-memory vectors run their slice phases on every
   // CTA of the cluster; otherwise the leader runs them alone
   Par par = leader_par(sm);
@@ -1864,7 +1946,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       if (threadIdx.x == 0) *abort_flag = 1;
     }
   }
-  cluster_barrier(C);
+  barrier();
   if (K == 1 && __ldcg(abort_flag)) return;
 
   // ---- steps ----
@@ -1916,7 +1998,11 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       micro_phase_big(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     if (prof) { c1 = clock64(); tp[0] += c1 - c0; c0 = c1; }
     if (profc) { const long long t = clock64(); pc_m += t - pc_t; pc_t = t; }
-    cluster_barrier(C);
+    if (a.sg > 1) {  // (owner of a live slice: every row of it was streamed this step)
+      if (sgo && s < nst && !__ldcg(abort_flag)) poll_moments();
+    } else {
+      barrier();
+    }
     if (prof) { c1 = clock64(); tp[1] += c1 - c0; c0 = c1; }
     if (profc) pc_b += clock64() - pc_t;
     // (K == 1: s < nst always, and an aborted slice has returned)
@@ -1938,7 +2024,7 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       if (!ok && threadIdx.x == 0) *abort_flag = 1;
       if (prof) { c1 = clock64(); tp[3] += c1 - c0; c0 = c1; }
     }
-    cluster_barrier(C);
+    barrier();
     if (prof) { c1 = clock64(); tp[4] += c1 - c0; c0 = c1; }
     if (K == 1 && __ldcg(abort_flag)) return;
   }
@@ -2147,6 +2233,7 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   static const bool dbg_packing = getenv("PK_DEBUG_PACKING") != nullptr;
   const bool autok = a.kps == 0;
   a.kps = 1;
+  a.sg = 0;
   if constexpr (!AD && G > 0) {
     // More slices than SMs (one CTA per slice, some SMs with one CTA and some
     // with two): pack K slices into clusters of C > K CTAs so that every CTA
@@ -2196,14 +2283,43 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
           C = cc;
           a.kps = kk;
         }
+      // Software groups (cooperative launch, no hardware cluster): the GPC
+      // packing limit does not apply, only the CTA slots of the whole chip,
+      // e.g. 256 slices as 37 groups of 8 CTAs x 7 slices on 296 slots.  The
+      // group barrier costs more than a cluster barrier: only a strictly
+      // lighter load than the best hardware packing qualifies.
+      static const bool no_sg = getenv("PK_NO_SG") != nullptr;
+      int occ = 0;
+      if (!no_sg && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 0;
+      }
+      const long long slots = (long long)occ * num_sms;
+      for (int cc = 2; cc <= 16 && !no_sg; ++cc)
+        for (int kk = 1; kk < cc; ++kk) {
+          const double load = (double)kk / cc;
+          if (load >= best - 1e-9 || (long long)(a.B + kk - 1) / kk * cc > slots) continue;
+          if ((long long)kk * a.m.nx < 32LL * cc * (NT / 32)) continue;
+          best = load;
+          C = cc;
+          a.kps = kk;
+          a.sg = cc;
+        }
     }
   }
-  if (dbg_packing) fprintf(stderr, "pk packing: B %d, cluster of %d CTAs x %d slices\n", a.B, C, a.kps);
+  const bool sg = a.sg > 1;
+  if (dbg_packing)
+    fprintf(stderr, "pk packing: B %d, %s of %d CTAs x %d slices\n", a.B,
+            a.sg > 1 ? "software group" : "cluster", C, a.kps);
   last_launch[0] = C;
   last_launch[1] = a.kps;
   last_launch[2] = a.local_smem;
-  last_launch[3] = 0;
-  if (C > 8) {
+  last_launch[3] = sg ? 1 : 0;
+  if (sg) {
+    e = cudaMemsetAsync(a.sg_cnt, 0, (size_t)((a.B + a.kps - 1) / a.kps) * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+  }
+  if (C > 8 && !sg) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
@@ -2213,10 +2329,15 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  if (sg) {  // every group's CTAs must be co-resident: the launch fails otherwise
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, a);

@@ -224,10 +224,10 @@ class Device:
 
     def last_launch(self):
         """Layout of this thread's last fine launch: (CTAs per cluster,
-        slices per cluster, slice vectors in shared memory)."""
+        slices per cluster, slice vectors in shared memory, software group)."""
         out = (C.c_int32 * 4)()
         self._rc(self.lib.pk_fine_last_launch(self.ctx, out), "pk_fine_last_launch")
-        return out[0], out[1], bool(out[2])
+        return out[0], out[1], bool(out[2]), bool(out[3])
 
     def check_stream(self, stream):
         """Raise this context's latched status after the work queued on

@@ -301,14 +301,17 @@ def test_batched_fine_matches_serial_windows():
         assert eq(g[b].cpu().numpy(), gg)
 
 
-@pytest.mark.parametrize("nv,B", [(64, 170), (128, 200), (128, 180)])
-def test_packed_clusters_match_one_slice_per_cluster(nv, B):
+@pytest.mark.parametrize("nv,B,sg", [(64, 170, None), (128, 200, None), (128, 180, None),
+                                     (128, 256, True), (64, 240, True)])
+def test_packed_clusters_match_one_slice_per_cluster(nv, B, sg):
     """More slices than SMs: the launcher packs K all-kinetic slices into
     thread-block clusters of C > K CTAs (e.g. 3 slices per 4 CTAs) when all
-    the clusters fit at once.  Step counts differ per slice and one slice
-    trips the solvability guard at entry; every other slice must come out
-    bitwise as with one slice per cluster (cluster_hint=1), and sampled slices
-    equal the oracle."""
+    the clusters fit at once, or -- when the GPC packing of clusters leaves no
+    lighter packing (256 slices) -- into software groups of C CTAs
+    (cooperative launch, moments through global memory, counter barriers).
+    Step counts differ per slice and one slice trips the solvability guard at
+    entry; every other slice must come out bitwise as with one slice per
+    cluster (cluster_hint=1), and sampled slices equal the oracle."""
     import torch
 
     from paper_2511_13386_b200.engine import Device, HybridKnobs, make_phase
@@ -337,12 +340,12 @@ def test_packed_clusters_match_one_slice_per_cluster(nv, B):
                  cluster_hint=hint)
         with pytest.raises(pk.SolvabilityViolation, match=f"slice {bad},"):
             dev.check()
-        Cc, K, on_chip = dev.last_launch()
+        Cc, K, on_chip, soft = dev.last_launch()
         assert on_chip
         if hint == 0:
-            assert 1 < K < Cc, (Cc, K)
+            assert 1 < K < Cc and (sg is None or soft == sg), (Cc, K, soft)
         else:
-            assert (Cc, K) == (1, 1)
+            assert (Cc, K, soft) == (1, 1, False)
         outs.append([x.cpu().numpy() for x in (rho, E, g)])
     keep = np.arange(B) != bad
     for x0, x1 in zip(*outs):

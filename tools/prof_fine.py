@@ -60,8 +60,8 @@ def main():
         print("   field cycles/step: src %d, pairwise2 %d, corr %d, cumsum %d, mean %d, sub %d"
               % tuple(int(x) // ns for x in c[8:14]))
         print("   slice vectors in shared memory:", bool(c[15]))
-        C, K, _ = ens.dev.last_launch()
-        print(f"   launch: clusters of {C} CTAs x {K} slices")
+        C, K, _, sg = ens.dev.last_launch()
+        print(f"   launch: {'software groups' if sg else 'clusters'} of {C} CTAs x {K} slices")
         if a.per_cta:
             ncta = (a.B + K - 1) // K * C
             pc = c[32:32 + 3 * ncta].reshape(ncta, 3)
@@ -72,8 +72,14 @@ def main():
             per_sm = np.bincount(pc[:, 2], minlength=148)
             for r in range(C):  # by rank within the group
                 sel = np.arange(ncta) % C == r
-                print(f"     rank {r}: micro median {np.median(mic[sel]):.0f}, "
+                print(f"     rank {r}: micro median {np.median(mic[sel]):.0f} max "
+                      f"{mic[sel].max():.0f}, bar median {np.median(bar[sel]):.0f}, "
                       f"SM-mates {np.mean(per_sm[pc[sel, 2]]):.2f}")
+            grp = np.arange(ncta) // C
+            gmax = np.array([mic[grp == q].max() for q in range(grp.max() + 1)])
+            gmin = np.array([mic[grp == q].min() for q in range(grp.max() + 1)])
+            print("   per-group micro max: min %d median %d max %d; spread (max-min) median %d"
+                  % (gmax.min(), np.median(gmax), gmax.max(), np.median(gmax - gmin)))
             for nmate in (1, 2):
                 sel = per_sm[pc[:, 2]] == nmate
                 if sel.any():
