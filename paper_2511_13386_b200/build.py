@@ -13,7 +13,7 @@ OUT = os.path.join(HERE, "libpk.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
+    "-O3", "-lineinfo", "-std=c++17", "--threads", "0",
     # exact IEEE double arithmetic in numpy's operation order: no contraction
     "--fmad=false",
     "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",

@@ -1103,31 +1103,50 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   };
 
   pump(S);
-  double c_vco = 0, c_dco = 0, c_J = 0, c_k1 = 0, c_k2 = 0;
-  int c_row = 0;
-  int cbase = p0 - 64;
-  for (int p = p0; p < p1;) {
-    if (p + 4 - cbase > 32) {
-      cbase = p;
-      const int pl = p + lane;
-      if (pl < p1) {
-        const int r = rowid(pl);
-        c_row = r;
-        // signed E-upwind factor: (g - g_nb) * (+-vco) reproduces both of the
-        // reference's forms bitwise (kinetic.py:176-187); 0 when E == 0
-        const int sg = __ldcg(v.vsg + r);
-        const double vco = __ldcg(v.vco + r);
-        c_vco = sg > 0 ? vco : (sg < 0 ? -vco : 0.0);
-        c_dco = __ldcg(v.dco + r);
-        c_J = __ldcg(v.gJ + r);
-        if (!kuni) {  // constant eps: kappa1/2 are per-slice scalars
-          c_k1 = __ldg(P.k1 + o + r);
-          c_k2 = __ldg(P.k2 + o + r);
-        }
-        // neighbour direction rides in the sign bit of the row id
-        c_row = sg > 0 ? r : -1 - r;
+  // per-row coefficients, one row per lane, 32 rows per batch
+  struct Coef {
+    double vco = 0, dco = 0, J = 0, k1 = 0, k2 = 0;
+    int row = 0;
+  };
+  auto load_batch = [&](int base, Coef& c) {
+    const int pl = base + lane;
+    if (pl < p1) {
+      const int r = rowid(pl);
+      // signed E-upwind factor: (g - g_nb) * (+-vco) reproduces both of the
+      // reference's forms bitwise (kinetic.py:176-187); 0 when E == 0
+      const int sg = __ldcg(v.vsg + r);
+      const double vco = __ldcg(v.vco + r);
+      c.vco = sg > 0 ? vco : (sg < 0 ? -vco : 0.0);
+      c.dco = __ldcg(v.dco + r);
+      c.J = __ldcg(v.gJ + r);
+      if (!kuni) {  // constant eps: kappa1/2 are per-slice scalars
+        c.k1 = __ldg(P.k1 + o + r);
+        c.k2 = __ldg(P.k2 + o + r);
       }
+      // neighbour direction rides in the sign bit of the row id
+      c.row = sg > 0 ? r : -1 - r;
     }
+  };
+  Coef cur, nxt;
+  int cbase = p0 - 64;
+  if (DENSE) {  // rows advance four per operation: batches at p0 + 32 n, the next one in flight
+    cbase = p0;
+    load_batch(p0, cur);
+    load_batch(p0 + 32, nxt);
+  }
+  for (int p = p0; p < p1;) {
+    if (DENSE) {
+      if (p - cbase >= 32) {
+        cur = nxt;
+        cbase += 32;
+        load_batch(cbase + 32, nxt);
+      }
+    } else if (p + 4 - cbase > 32) {
+      cbase = p;
+      load_batch(p, cur);
+    }
+    const double c_vco = cur.vco, c_dco = cur.dco, c_J = cur.J, c_k1 = cur.k1, c_k2 = cur.k2;
+    const int c_row = cur.row;
     // entries of this operation (up to four, within the ring window)
     int nent, my_q, last_q;
     if (DENSE) {
