@@ -233,6 +233,9 @@ pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
         std::memcmp(&xM[j], &p, 8) != 0)
       m.mirror = 0;
   }
+  m.xplane = 1;
+  for (int j = 0; j < nv; ++j)
+    if (std::memcmp(&h[j], &h[(size_t)(j / nvyz) * nvyz], 8) != 0) m.xplane = 0;
   // pairwise plans: x sums (nx terms), and for 1D-3V rows the folded velocity
   // block ((nvx/2) nvy nvz terms) and the middle xi plane (nvy nvz terms)
   PwPlan plan[3];
@@ -369,8 +372,13 @@ int32_t pk_fine_propagate(pk_ctx* c, int32_t B, double* rho, double* E, double* 
   int C = cluster_hint;
   if (C <= 0) {
     C = 1;
-    const int slots = 2 * c->num_sms;
-    while (C < 8 && B * C * 2 <= slots && c->m.nx >= (C * 2) * 8 * 4) C *= 2;
+    if (c->m.nvyz > 1 && c->m.nv > 256) {  // (the big-row layout, launch_fine)
+      // big rows: one CTA per row at one CTA per SM, >= 2 rows per CTA
+      while (C < 8 && B * C * 2 <= c->num_sms && c->m.nx >= (C * 2) * 2) C *= 2;
+    } else {
+      const int slots = 2 * c->num_sms;
+      while (C < 8 && B * C * 2 <= slots && c->m.nx >= (C * 2) * 8 * 4) C *= 2;
+    }
   }
   a.nwarp_total = C * 8;
   a.kps = cluster_hint > 0 ? 1 : 0;  // 0: the launcher may pack slices per cluster

@@ -12,6 +12,7 @@ namespace pk {
 struct MeshDev {
   int nx, nv;
   int nvyz;            // nvy * nvz: stride of the xi axis within a row (1: 1D-x/1D-v)
+  int xplane;          // xi constant on each xi plane: vx[c] == vx[(c / nvyz) nvyz] bit for bit
   int mirror;          // vx[nv-1-j] == -vx[j], M[nv-1-j] == M[j] and xiM[j] == vx[j]*M[j]
                        // bit for bit (the reference's mirrored grid, mesh.py:31-44,136)
   double dx, rdx, two_dx, dvx, dv3, m0, m2;
@@ -48,6 +49,7 @@ struct FineArgs {
   int sg;                // > 1: the "cluster" is a software group of sg CTAs (no hardware
                          // cluster; moments through global memory, barriers on sg_cnt)
   unsigned* sg_cnt;      // [B] per-group arrival counters (zeroed by the launcher)
+  int bigc;              // big rows, one CTA per row through shared-memory row buffers (launcher)
   // state
   double* rho;           // [B*nx] in/out
   double* E;             // [B*nx] out: field at the end (also working E)

@@ -1566,6 +1566,171 @@ __device__ void micro_phase_big(const FineArgs& a, const SliceView& v, const Sme
   }
 }
 
+// Big rows, one CTA per row (FineArgs::bigc; nvy nvz a multiple of the CTA
+// width, mirrored grid with xi constant on each xi plane -- the reference's
+// 32 x 16 x 16 default): the CTA's rows stream through two shared-memory row
+// buffers filled by single TMA bulk copies, the next row landing while the
+// current one is worked on; M and the per-plane xi sit in shared memory.
+// Thread t owns the (vy, vz) columns t + NT w and walks each along the xi
+// axis, so the xi neighbours c -/+ S are its own previous / next nodes (held
+// in registers) and the updated node can overwrite the staged input in place.
+// The x neighbour (row i+1 for xi < 0, i-1 for xi > 0) comes from L2.  Same
+// operations in the same order as big_micro_row (kinetic.py:148-224), the
+// zero upwind term skipped as in the fast layouts (equal up to the sign of
+// zero); the row moments then run as one block-wide pairwise sweep over the
+// staged output (the folded block's plan and, for odd nvx, the middle plane's),
+// bitwise as big_bracket.
+constexpr int BIGC_NXI = 32;  // xi planes (nvx) of the layout: a column walk in registers
+
+template <int NT>
+__device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
+                                 const double* gin, double* gout, int crank, int C, double* rbuf,
+                                 const double* sM, const double* sxi, uint64_t* mbar,
+                                 uint32_t& qbase) {
+  const MeshDev& m = a.m;
+  const int nx = m.nx, nv = m.nv, S = m.nvyz, nvx = nv / S, F = (nvx / 2) * S;
+  const int nk = __ldcg(v.nk);
+  const bool dense = nk == nx;
+  const int p0 = (int)(((long long)crank * nk) / C), p1 = (int)(((long long)(crank + 1) * nk) / C);
+  if (p0 >= p1) return;
+  const PhaseDev& P = a.ph[ph];
+  const size_t o = (size_t)v.b * nx;
+  const int tid = threadIdx.x;
+  const bool sq = a.adaptation != 0;
+  const int hx = nvx / 2;  // planes jx < hx: xi < 0; jx >= nvx - hx: xi > 0
+  auto rowid = [&](int p) { return dense ? p : __ldcg(v.klist + p); };
+  auto coef = [&](int i) {
+    RowCoef rc;
+    rc.vsg = __ldcg(v.vsg + i);
+    rc.vco = __ldcg(v.vco + i);
+    rc.dc = __ldcg(v.dco + i);
+    rc.J = __ldcg(v.gJ + i);
+    rc.k1 = P.k1[o + i];
+    rc.k2 = P.k2[o + i];
+    return rc;
+  };
+  const uint32_t bytes = (uint32_t)nv * 8;
+  // row q of this phase goes to slot (qbase + q) & 1 at parity ((qbase + q) >> 1) & 1
+  auto issue = [&](int q, int i) {
+    if (tid == 0) {
+      const uint32_t Q = qbase + (uint32_t)q;
+      mbar_expect_tx(mbar + (Q & 1), bytes);
+      bulk_g2s(rbuf + (size_t)(Q & 1) * nv, gin + (size_t)i * nv, bytes, mbar + (Q & 1));
+    }
+  };
+  if (tid == 0) fence_proxy_async_global();  // rows written by the generic proxy, read by TMA
+  int i_cur = rowid(p0);
+  issue(0, i_cur);
+  int i_nxt = p0 + 1 < p1 ? rowid(p0 + 1) : 0;
+  if (p0 + 1 < p1) issue(1, i_nxt);
+  RowCoef rc = coef(i_cur);
+  const double dx = m.dx, rdx = m.rdx;
+  for (int p = p0; p < p1; ++p) {
+    const int q = p - p0;
+    const uint32_t Q = qbase + (uint32_t)q;
+    double* rb = rbuf + (size_t)(Q & 1) * nv;
+    const int i = i_cur;
+    // next row's id and coefficients ride ahead of the current row's work
+    const int i_n2 = p + 2 < p1 ? rowid(p + 2) : 0;
+    RowCoef rn = rc;
+    if (p + 1 < p1) rn = coef(i_nxt);
+    const double* gp = gin + (size_t)wrap(i - 1, nx) * nv;
+    const double* gn = gin + (size_t)wrap(i + 1, nx) * nv;
+    double* out = gout + (size_t)i * nv;
+    const double Ep = rc.vsg > 0 ? rc.vco : 0.0;
+    const double Em = rc.vsg < 0 ? rc.vco : 0.0;
+    long long* const dbg = (a.prof && v.b == 0 && crank == 0 && tid == 0) ? a.prof + 24 : nullptr;
+    long long t0 = dbg ? clock64() : 0;
+    auto tick = [&](int k) {
+      if (dbg) {
+        const long long t1 = clock64();
+        dbg[k] += t1 - t0;
+        t0 = t1;
+      }
+    };
+    // two threads per (vy, vz) column, lanes l and l ^ 16 of one warp: the
+    // lower half (h = 0) walks planes 0 .. H-1 (xi < 0), the upper half planes
+    // H .. 2H-1 (xi > 0); the xi neighbours across the split and the fold
+    // partners (plane jx and 2H-1-jx) are exchanged by shuffles
+    constexpr int H = BIGC_NXI / 2;
+    const int lane = tid & 31, h = lane >> 4;
+    for (int col = (tid >> 5) * 16 + (lane & 15); col < S; col += NT / 2) {
+      // the column half's x neighbours (independent L2 loads), then its staged
+      // input, then every node's update (no memory operation in between, so the
+      // nodes' FP64 chains interleave), then the stores
+      const double* xr = (h == 0 ? gn : gp) + (size_t)(h * H) * S + col;
+      const double* gr = rb + (size_t)(h * H) * S + col;
+      double xn[H], gc[H];
+#pragma unroll
+      for (int k = 0; k < H; ++k) xn[k] = __ldcg(xr + (size_t)k * S);
+      if (col < 16 * (NT / 32)) mbar_wait(mbar + (Q & 1), (Q >> 1) & 1);
+#pragma unroll
+      for (int k = 0; k < H; ++k) gc[k] = gr[k * S];
+      // g of plane H (for the lower half's last node) / plane H-1 (upper's first)
+      const double gx = __shfl_xor_sync(FULL, h == 0 ? gc[H - 1] : gc[0], 16);
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        const int jx = h * H + k;
+        const double g = gc[k];
+        const double xi = sxi[jx];
+        double w = h == 0 ? xi * (xn[k] - g) : xi * (g - xn[k]);
+        w = qdiv(w, dx, rdx);
+        const double gm = k > 0 ? gc[k > 0 ? k - 1 : 0] : (h == 0 ? 0.0 : gx);
+        const double dm = jx == 0 ? g : g - gm;
+        w = w + dm * Ep;
+        const double gq = k + 1 < H ? gc[k + 1 < H ? k + 1 : k] : (h == 0 ? gx : 0.0);
+        const double dp = jx + 1 == BIGC_NXI ? -g : gq - g;
+        w = w + dp * Em;
+        const double Mc = sM[jx * S + col];
+        w = w - Mc * rc.dc;
+        const double forcing = w + (xi * Mc) * rc.J;
+        xn[k] = rc.k1 * g - rc.k2 * forcing;
+      }
+      double* outc = out + (size_t)(h * H) * S + col;
+#pragma unroll
+      for (int k = 0; k < H; ++k) __stcg(outc + (size_t)k * S, xn[k]);
+      // fold terms of the row moments (big_bracket: q(j) + q(mirror j)), over
+      // this column's own staged input: the lower half writes the <xi g'>
+      // terms of fold planes 0 .. H-1 at [0, F), the upper half the <g'^2>
+      // terms at [F, 2F) (plane jx <-> 2H-1-jx: lower k <-> upper H-1-k)
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        const double y = __shfl_xor_sync(FULL, xn[H - 1 - k], 16);
+        if (h == 0) {
+          rb[k * S + col] = sxi[k] * xn[k] + sxi[BIGC_NXI - 1 - k] * y;
+        } else if (sq) {
+          // fold plane H-1-k: lower plane H-1-k (received) and upper plane H+k
+          rb[F + (H - 1 - k) * S + col] = y * y + xn[k] * xn[k];
+        }
+      }
+    }
+    tick(1);
+    __syncthreads();
+    tick(2);
+    double bx, bsq = 0.0;
+    if (sq)
+      block_pairwise2([&](int j) { return rb[j]; }, [&](int j) { return rb[F + j]; }, *m.plan_f,
+                      sm.red, bx, bsq);
+    else
+      bx = block_pairwise([&](int j) { return rb[j]; }, *m.plan_f, sm.red);
+    tick(4);
+    if (dbg) dbg[5] += 1;
+    if (tid == 0) {
+      v.fl_w[i] = bx * m.dv3;
+      if (sq) v.sq_w[i] = bsq * m.dv3;
+    }
+    // (block_pairwise ends on a barrier: the buffer is free) refill it with row p + 2
+    if (p + 2 < p1) {
+      if (tid == 0) fence_proxy_async_smem();  // generic writes to the slot, then TMA
+      issue(q + 2, i_n2);
+    }
+    i_cur = i_nxt;
+    i_nxt = i_n2;
+    rc = rn;
+  }
+  qbase += (uint32_t)(p1 - p0);
+}
+
 // Prologue row pass: (optionally lift and) copy the input rows into the
 // step-0 input buffer and compute their moments.
 template <int T>
@@ -1749,7 +1914,7 @@ __device__ __forceinline__ void group_barrier(unsigned* cnt, int C, unsigned& n)
 // AD: adaptation on (hybrid) or off (all-kinetic, compiled without the
 // labels / lifts / row lists of the hybrid slice phase)
 template <int T, int S, int G, int NT, bool AD>
-__global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
+__global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs a) {
   // ring row stride (doubles); G > 0: per-warp G8 rings, G < 0: CTA-wide
   // producer/consumer ring of the GS layout with SEG = -G
   constexpr int RSN = G > 0 ? 16 * G + 8 : (G < 0 ? 64 * (-G) + 8 : 32 * (T > 0 ? T : 1));
@@ -1810,7 +1975,16 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
     sm.misc = reinterpret_cast<int*>(p); p += 64 * 4;
     sm.wrow = reinterpret_cast<double*>(p);
     if (T == 0) p += (size_t)nwpc * nv * 8;       // generic-layout row scratch
-    if (T < 0) p += (size_t)nwpc * BIG_SCR * 8;   // big rows: plan scratch
+    if (T < 0 && !a.bigc) p += (size_t)nwpc * BIG_SCR * 8;   // big rows: plan scratch
+    if (T < 0 && a.bigc) {
+      // big rows, one CTA per row: 2 row buffers, M, xi per plane; the plan
+      // scratch of the per-warp row operations (prologue, lifts: never during
+      // a micro phase) lives in the row buffers
+      p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+      ring = reinterpret_cast<double*>(p);
+      sm.wrow = ring;
+      p += ((size_t)3 * nv + nv / m.nvyz + 1) / 2 * 16;
+    }
     if (T > 0) {
       ring = reinterpret_cast<double*>(p);
       p += (size_t)(G < 0 ? 1 : nwpc) * S * RSN * 8;
@@ -1831,7 +2005,13 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
         sm.w2[j] = m.w2[j];
       }
     if (T > 0 && threadIdx.x < (G < 0 ? 2 * S : nwpc * S)) mbar_init(mbar + threadIdx.x, 1);
-    if (T > 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (T < 0 && a.bigc) {
+      if (threadIdx.x < 2) mbar_init(mbar + threadIdx.x, 1);
+      for (int j = threadIdx.x; j < nv; j += blockDim.x) ring[2 * (size_t)nv + j] = m.M[j];
+      for (int j = threadIdx.x; j < nv / m.nvyz; j += blockDim.x)
+        ring[3 * (size_t)nv + j] = m.vx[(size_t)j * m.nvyz];
+    }
+    if (T > 0 || (T < 0 && a.bigc)) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
@@ -2013,6 +2193,9 @@ __global__ void __launch_bounds__(NT, 2) fine_kernel(const FineArgs a) {
       micro_phase_tma<T, S>(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg, ring_w, mbar_w, qbase);
     else if constexpr (T == 0)
       micro_phase_gen(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
+    else if (a.bigc)
+      micro_phase_bigc<NT>(a, v, sm, ph, buf(s), buf(s + 1), crank, C, ring, ring + 2 * (size_t)nv,
+                           ring + 3 * (size_t)nv, mbar, qbase);
     else
       micro_phase_big(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     if (prof) { c1 = clock64(); tp[0] += c1 - c0; c0 = c1; }
@@ -2199,6 +2382,13 @@ static size_t base_smem(int nv, int T, int S, int G, int NT) {
   return s;
 }
 
+// the one-CTA-per-row big-row layout (micro_phase_bigc): 32 xi planes of
+// nvy nvz columns, a multiple of 256 (two threads per column at 512 threads),
+// mirrored grid with xi constant on each plane
+static bool bigc_layout(const MeshDev& m) {
+  return m.nvyz > 1 && m.nvyz % 256 == 0 && m.nv / m.nvyz == BIGC_NXI && m.mirror && m.xplane;
+}
+
 static size_t local_smem(int nx, int adaptation) {
   return adaptation ? (size_t)nx * (NLOC_D * 8 + NLOC_B) + 16
                     : (size_t)nx * (NLOC_DK * 8 + NLOC_BK) + 16;
@@ -2213,7 +2403,15 @@ void fine_last_launch(int out[4]) {
 
 template <int T, int S, int G, int NT, bool AD>
 static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
-  const size_t base = base_smem(a.m.nv, T, S, G, NT);
+  // big rows: one CTA per row through shared-memory row buffers when two rows
+  // fit (one CTA per SM); else the warp-per-row layout on global rows
+  static const bool no_bigc = getenv("PK_NO_BIGC") != nullptr;
+  const size_t rowbufs = ((size_t)3 * a.m.nv + a.m.nv / a.m.nvyz + 1) / 2 * 16 + 16;
+  const size_t scr = (NT / 32) * (size_t)BIG_SCR * 8;  // (T < 0) plan scratch, aliased under bigc
+  a.bigc = T < 0 && NT == 512 && !no_bigc && bigc_layout(a.m) &&
+           base_smem(a.m.nv, T, S, G, NT) - scr + rowbufs + 16 * 8 <= 226 * 1024 &&
+           (size_t)(NT / 32) * BIG_SCR <= 2 * (size_t)a.m.nv;
+  const size_t base = base_smem(a.m.nv, T, S, G, NT) + (a.bigc ? rowbufs - scr : 0);
   // slice vectors on chip when they fit: two CTAs per SM when the grid needs
   // them, the whole SM's shared memory when the grid has one CTA per SM
   static int num_sms = 0;
@@ -2224,9 +2422,10 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   }
   const size_t need = base + local_smem(a.m.nx, a.adaptation);
   // half the cluster if that puts the slice vectors on chip (one CTA per SM)
-  if (need > 112 * 1024 && need <= 226 * 1024 && C >= 2 && (size_t)a.B * (C / 2) <= (size_t)num_sms)
+  if (!a.bigc && need > 112 * 1024 && need <= 226 * 1024 && C >= 2 &&
+      (size_t)a.B * (C / 2) <= (size_t)num_sms)
     C /= 2;
-  const size_t limit = (size_t)a.B * C <= (size_t)num_sms ? 226 * 1024 : 112 * 1024;
+  const size_t limit = a.bigc || (size_t)a.B * C <= (size_t)num_sms ? 226 * 1024 : 112 * 1024;
   // test hook: PK_FORCE_GLOBAL_SLICE=1 keeps the slice vectors in global
   // memory (whole scan buffer on chip), =2 also cuts the scan buffer to 48
   // doubles (chunked scan), so small golden cases exercise the large-nx paths
@@ -2333,7 +2532,7 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   last_launch[0] = C;
   last_launch[1] = a.kps;
   last_launch[2] = a.local_smem;
-  last_launch[3] = sg ? 1 : 0;
+  last_launch[3] = sg ? 1 : (a.bigc ? 2 : 0);
   if (sg) {
     e = cudaMemsetAsync(a.sg_cnt, 0, (size_t)((a.B + a.kps - 1) / a.kps) * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
@@ -2405,6 +2604,7 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   if (a.m.nvyz > 1) {  // 1D-3V rows: generic layout up to 256 nodes, big rows beyond
     if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
+    if (bigc_layout(a.m) && !getenv("PK_NO_BIGC")) return launch_T<-1, 1, 0, 512>(a, C, st);
     return launch_T<-1, 1, 0, 256>(a, C, st);
   }
   if ((a.m.nv == 64 || a.m.nv == 128) && !a.m.mirror)  // G8 needs the mirrored grid

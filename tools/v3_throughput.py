@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--nvz", type=int, default=16)
     ap.add_argument("--B", type=int, default=16)
     ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     import torch
 
@@ -43,7 +44,10 @@ def main():
     ens = Ensemble(m, [0.5] * a.B, [p.dt] * a.B, [rb] * a.B)
     rho_d = torch.from_numpy(np.tile(rho, (a.B, 1))).cuda()
     g_d = torch.from_numpy(np.tile(g0.reshape(1, a.nx, -1), (a.B, 1, 1))).cuda()
-    for rep in range(3):
+    cnt = torch.zeros(32 + 3 * 1024, dtype=torch.int64, device="cuda")
+    ens.dev.lib.pk_debug_profile(ens.dev.ctx, cnt.data_ptr())
+    for rep in range(a.reps):
+        cnt.zero_()
         ens.load(rho_d, g_d)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -55,6 +59,15 @@ def main():
         print(f"rep {rep}: {ms:.2f} ms, {upd / ms * 1e3:.3e} cell-updates/s, "
               f"{16 * upd / ms / 1e6:.0f} GB/s algorithmic (grid {a.nx} x {a.nvx}x{a.nvy}x{a.nvz}, "
               f"B={a.B}, {a.steps} steps)")
+        c = cnt.cpu().numpy()
+        ns = max(int(c[5]), 1)
+        print("   slice0 cycles/step: micro %d, bar %d, finish %d, prepare %d, bar %d"
+              % tuple(int(x) // ns for x in c[:5]))
+        nr = max(int(c[29]), 1)
+        print("   bigc row (CTA 0 of slice 0), cycles/row: wait %d, compute %d, sync %d, "
+              "writeback %d, moments %d over %d rows" % (*(int(x) // nr for x in c[24:29]), nr))
+        print("   launch (CTAs per cluster, slices per cluster, on chip, group/bigc):",
+              ens.dev.last_launch())
 
 
 if __name__ == "__main__":
