@@ -1566,38 +1566,49 @@ __device__ void micro_phase_big(const FineArgs& a, const SliceView& v, const Sme
   }
 }
 
-// Big rows, one CTA per row (FineArgs::bigc; nvy nvz a multiple of the CTA
-// width, mirrored grid with xi constant on each xi plane -- the reference's
-// 32 x 16 x 16 default): the CTA's rows stream through two shared-memory row
-// buffers filled by single TMA bulk copies, the next row landing while the
-// current one is worked on; M and the per-plane xi sit in shared memory.
-// Thread t owns the (vy, vz) columns t + NT w and walks each along the xi
-// axis, so the xi neighbours c -/+ S are its own previous / next nodes (held
-// in registers) and the updated node can overwrite the staged input in place.
-// The x neighbour (row i+1 for xi < 0, i-1 for xi > 0) comes from L2.  Same
-// operations in the same order as big_micro_row (kinetic.py:148-224), the
-// zero upwind term skipped as in the fast layouts (equal up to the sign of
-// zero); the row moments then run as one block-wide pairwise sweep over the
-// staged output (the folded block's plan and, for odd nvx, the middle plane's),
-// bitwise as big_bracket.
-constexpr int BIGC_NXI = 32;  // xi planes (nvx) of the layout: a column walk in registers
+// Big rows, one CTA per row (FineArgs::bigc): the reference's default 1D-3V
+// grid, 32 xi planes of nvy nvz = 256 (vy, vz) columns, mirrored, xi constant
+// on each plane.  The CTA's rows stream through two shared-memory row buffers
+// filled by single TMA bulk copies, the next row landing while the current
+// one is worked on; M and the per-plane xi sit in shared memory.
+//
+// The thread layout follows the row moments.  <q> folds plane jx with plane
+// 31-jx and sums the 4096 folded terms pairwise (mesh.py:95-133): 32 leaves
+// of 128 (fold plane jx = l / 2, column block l % 2), each leaf eight
+// interleaved accumulators (columns k + 8 m, m = 0..15, in order) combined by
+// a butterfly, then a perfectly balanced tree over the leaves.  Thread (l, k)
+// -- warp l / 4, lanes 8 (l % 4) + k -- updates exactly the nodes of its
+// accumulator: columns 128 (l % 2) + k + 8 m of planes jx and 31 - jx (xi < 0
+// and its mirror xi > 0), 32 nodes, and accumulates its fold terms in
+// registers in leaf order; the leaf butterfly is group_leaf's (shuffles in
+// the 8-lane group), the tree a 32-lane butterfly of warp 0 over the leaves
+// in order.  One barrier per row.  Node updates: the operations of
+// big_micro_row (kinetic.py:148-224) in its order, the xi neighbours c -/+ S
+// from the staged row, the x neighbour (row i+1 for xi < 0, i-1 for xi > 0)
+// from L2, the zero upwind term skipped as in the fast layouts (equal up to
+// the sign of zero).
+constexpr int BIGC_NXI = 32;   // xi planes
+constexpr int BIGC_S = 256;    // (vy, vz) columns per plane
 
-template <int NT>
 __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                  const double* gin, double* gout, int crank, int C, double* rbuf,
                                  const double* sM, const double* sxi, uint64_t* mbar,
                                  uint32_t& qbase) {
+  constexpr int S = BIGC_S, X = BIGC_NXI, NM = 16;
   const MeshDev& m = a.m;
-  const int nx = m.nx, nv = m.nv, S = m.nvyz, nvx = nv / S, F = (nvx / 2) * S;
+  const int nx = m.nx, nv = m.nv;
   const int nk = __ldcg(v.nk);
   const bool dense = nk == nx;
   const int p0 = (int)(((long long)crank * nk) / C), p1 = (int)(((long long)(crank + 1) * nk) / C);
   if (p0 >= p1) return;
   const PhaseDev& P = a.ph[ph];
   const size_t o = (size_t)v.b * nx;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int l = tid >> 3, k = lane & 7;  // leaf, accumulator
+  const int jx = l >> 1, jm = X - 1 - jx;
+  const int col0 = (l & 1) * 128 + k;
   const bool sq = a.adaptation != 0;
-  const int hx = nvx / 2;  // planes jx < hx: xi < 0; jx >= nvx - hx: xi > 0
+  const double xl = sxi[jx], xh = sxi[jm];
   auto rowid = [&](int p) { return dense ? p : __ldcg(v.klist + p); };
   auto coef = [&](int i) {
     RowCoef rc;
@@ -1628,102 +1639,106 @@ __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Sm
   for (int p = p0; p < p1; ++p) {
     const int q = p - p0;
     const uint32_t Q = qbase + (uint32_t)q;
-    double* rb = rbuf + (size_t)(Q & 1) * nv;
+    const double* rb = rbuf + (size_t)(Q & 1) * nv;
     const int i = i_cur;
     // next row's id and coefficients ride ahead of the current row's work
     const int i_n2 = p + 2 < p1 ? rowid(p + 2) : 0;
     RowCoef rn = rc;
     if (p + 1 < p1) rn = coef(i_nxt);
-    const double* gp = gin + (size_t)wrap(i - 1, nx) * nv;
-    const double* gn = gin + (size_t)wrap(i + 1, nx) * nv;
-    double* out = gout + (size_t)i * nv;
     const double Ep = rc.vsg > 0 ? rc.vco : 0.0;
     const double Em = rc.vsg < 0 ? rc.vco : 0.0;
-    long long* const dbg = (a.prof && v.b == 0 && crank == 0 && tid == 0) ? a.prof + 24 : nullptr;
-    long long t0 = dbg ? clock64() : 0;
-    auto tick = [&](int k) {
-      if (dbg) {
-        const long long t1 = clock64();
-        dbg[k] += t1 - t0;
-        t0 = t1;
-      }
-    };
-    // two threads per (vy, vz) column, lanes l and l ^ 16 of one warp: the
-    // lower half (h = 0) walks planes 0 .. H-1 (xi < 0), the upper half planes
-    // H .. 2H-1 (xi > 0); the xi neighbours across the split and the fold
-    // partners (plane jx and 2H-1-jx) are exchanged by shuffles
-    constexpr int H = BIGC_NXI / 2;
-    const int lane = tid & 31, h = lane >> 4;
-    for (int col = (tid >> 5) * 16 + (lane & 15); col < S; col += NT / 2) {
-      // the column half's x neighbours (independent L2 loads), then its staged
-      // input, then every node's update (no memory operation in between, so the
-      // nodes' FP64 chains interleave), then the stores
-      const double* xr = (h == 0 ? gn : gp) + (size_t)(h * H) * S + col;
-      const double* gr = rb + (size_t)(h * H) * S + col;
-      double xn[H], gc[H];
+    // x neighbours from L2 first (row i+1 on the lower plane, i-1 on the upper)
+    const double* gnl = gin + (size_t)wrap(i + 1, nx) * nv + jx * S + col0;
+    const double* gph = gin + (size_t)wrap(i - 1, nx) * nv + jm * S + col0;
+    double xa[NM], xb[NM];
 #pragma unroll
-      for (int k = 0; k < H; ++k) xn[k] = __ldcg(xr + (size_t)k * S);
-      if (col < 16 * (NT / 32)) mbar_wait(mbar + (Q & 1), (Q >> 1) & 1);
+    for (int u = 0; u < NM; ++u) {
+      xa[u] = __ldcg(gnl + 8 * u);
+      xb[u] = __ldcg(gph + 8 * u);
+    }
+    mbar_wait(mbar + (Q & 1), (Q >> 1) & 1);
+    const double* rl = rb + jx * S + col0;
+    const double* rh = rb + jm * S + col0;
+    const double* Ml = sM + jx * S + col0;
+    const double* Mh = sM + jm * S + col0;
+    double a1 = 0.0, a2 = 0.0;
 #pragma unroll
-      for (int k = 0; k < H; ++k) gc[k] = gr[k * S];
-      // g of plane H (for the lower half's last node) / plane H-1 (upper's first)
-      const double gx = __shfl_xor_sync(FULL, h == 0 ? gc[H - 1] : gc[0], 16);
-#pragma unroll
-      for (int k = 0; k < H; ++k) {
-        const int jx = h * H + k;
-        const double g = gc[k];
-        const double xi = sxi[jx];
-        double w = h == 0 ? xi * (xn[k] - g) : xi * (g - xn[k]);
+    for (int u = 0; u < NM; ++u) {
+      const int c = 8 * u;
+      double lo, hi;
+      {  // plane jx, xi < 0: x-upwind from row i+1; zero xi-inflow below plane 0
+        const double g = rl[c];
+        double w = xl * (xa[u] - g);
         w = qdiv(w, dx, rdx);
-        const double gm = k > 0 ? gc[k > 0 ? k - 1 : 0] : (h == 0 ? 0.0 : gx);
-        const double dm = jx == 0 ? g : g - gm;
+        const double gb = rl[c - S];  // (jx = 0: before the row, inside shared memory, unused)
+        const double dm = jx == 0 ? g : g - gb;
         w = w + dm * Ep;
-        const double gq = k + 1 < H ? gc[k + 1 < H ? k + 1 : k] : (h == 0 ? gx : 0.0);
-        const double dp = jx + 1 == BIGC_NXI ? -g : gq - g;
+        const double dp = rl[c + S] - g;  // (jx + 1 <= 16 < X)
         w = w + dp * Em;
-        const double Mc = sM[jx * S + col];
+        const double Mc = Ml[c];
         w = w - Mc * rc.dc;
-        const double forcing = w + (xi * Mc) * rc.J;
-        xn[k] = rc.k1 * g - rc.k2 * forcing;
+        const double forcing = w + (xl * Mc) * rc.J;
+        lo = rc.k1 * g - rc.k2 * forcing;
       }
-      double* outc = out + (size_t)(h * H) * S + col;
-#pragma unroll
-      for (int k = 0; k < H; ++k) __stcg(outc + (size_t)k * S, xn[k]);
-      // fold terms of the row moments (big_bracket: q(j) + q(mirror j)), over
-      // this column's own staged input: the lower half writes the <xi g'>
-      // terms of fold planes 0 .. H-1 at [0, F), the upper half the <g'^2>
-      // terms at [F, 2F) (plane jx <-> 2H-1-jx: lower k <-> upper H-1-k)
-#pragma unroll
-      for (int k = 0; k < H; ++k) {
-        const double y = __shfl_xor_sync(FULL, xn[H - 1 - k], 16);
-        if (h == 0) {
-          rb[k * S + col] = sxi[k] * xn[k] + sxi[BIGC_NXI - 1 - k] * y;
-        } else if (sq) {
-          // fold plane H-1-k: lower plane H-1-k (received) and upper plane H+k
-          rb[F + (H - 1 - k) * S + col] = y * y + xn[k] * xn[k];
-        }
+      {  // plane 31 - jx, xi > 0: x-upwind from row i-1; zero inflow above plane 31
+        const double g = rh[c];
+        double w = xh * (g - xb[u]);
+        w = qdiv(w, dx, rdx);
+        const double dm = g - rh[c - S];  // (jm - 1 >= 15 >= 0)
+        w = w + dm * Ep;
+        const double gq = rh[c + S];  // (jm = 31: past the row, inside shared memory, unused)
+        const double dp = jm + 1 == X ? -g : gq - g;
+        w = w + dp * Em;
+        const double Mc = Mh[c];
+        w = w - Mc * rc.dc;
+        const double forcing = w + (xh * Mc) * rc.J;
+        hi = rc.k1 * g - rc.k2 * forcing;
+      }
+      xa[u] = lo;
+      xb[u] = hi;
+      // fold terms (q(j) + q(mirror j)), accumulated in leaf order
+      const double f1 = xl * lo + xh * hi;
+      a1 = u == 0 ? f1 : a1 + f1;
+      if (sq) {
+        const double f2 = lo * lo + hi * hi;
+        a2 = u == 0 ? f2 : a2 + f2;
       }
     }
-    tick(1);
-    __syncthreads();
-    tick(2);
-    double bx, bsq = 0.0;
-    if (sq)
-      block_pairwise2([&](int j) { return rb[j]; }, [&](int j) { return rb[F + j]; }, *m.plan_f,
-                      sm.red, bx, bsq);
-    else
-      bx = block_pairwise([&](int j) { return rb[j]; }, *m.plan_f, sm.red);
-    tick(4);
-    if (dbg) dbg[5] += 1;
-    if (tid == 0) {
-      v.fl_w[i] = bx * m.dv3;
-      if (sq) v.sq_w[i] = bsq * m.dv3;
+    double* ol = gout + (size_t)i * nv + jx * S + col0;
+    double* oh = gout + (size_t)i * nv + jm * S + col0;
+#pragma unroll
+    for (int u = 0; u < NM; ++u) {
+      __stcg(ol + 8 * u, xa[u]);
+      __stcg(oh + 8 * u, xb[u]);
     }
-    // (block_pairwise ends on a barrier: the buffer is free) refill it with row p + 2
-    if (p + 2 < p1) {
-      if (tid == 0) fence_proxy_async_smem();  // generic writes to the slot, then TMA
-      issue(q + 2, i_n2);
+    // leaf: group_leaf's butterfly over the eight accumulators
+    a1 = a1 + __shfl_xor_sync(FULL, a1, 1);
+    a1 = a1 + __shfl_xor_sync(FULL, a1, 2);
+    a1 = a1 + __shfl_xor_sync(FULL, a1, 4);
+    if (sq) {
+      a2 = a2 + __shfl_xor_sync(FULL, a2, 1);
+      a2 = a2 + __shfl_xor_sync(FULL, a2, 2);
+      a2 = a2 + __shfl_xor_sync(FULL, a2, 4);
     }
+    if (k == 0) {
+      sm.red[l] = a1;
+      sm.red[32 + l] = a2;
+    }
+    __syncthreads();  // leaves ready; every thread is done with the staged row
+    if (tid < 32) {   // balanced tree over the 32 leaves in order
+      double r1 = sm.red[lane], r2 = sm.red[32 + lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        r1 = r1 + __shfl_xor_sync(FULL, r1, d);
+        if (sq) r2 = r2 + __shfl_xor_sync(FULL, r2, d);
+      }
+      if (tid == 0) {
+        v.fl_w[i] = r1 * m.dv3;
+        if (sq) v.sq_w[i] = r2 * m.dv3;
+      }
+      __syncwarp();
+    }
+    if (p + 2 < p1) issue(q + 2, i_n2);  // (the staged row was only read: no proxy fence)
     i_cur = i_nxt;
     i_nxt = i_n2;
     rc = rn;
@@ -2194,8 +2209,8 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
     else if constexpr (T == 0)
       micro_phase_gen(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     else if (a.bigc)
-      micro_phase_bigc<NT>(a, v, sm, ph, buf(s), buf(s + 1), crank, C, ring, ring + 2 * (size_t)nv,
-                           ring + 3 * (size_t)nv, mbar, qbase);
+      micro_phase_bigc(a, v, sm, ph, buf(s), buf(s + 1), crank, C, ring, ring + 2 * (size_t)nv,
+                       ring + 3 * (size_t)nv, mbar, qbase);
     else
       micro_phase_big(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     if (prof) { c1 = clock64(); tp[0] += c1 - c0; c0 = c1; }
@@ -2383,10 +2398,9 @@ static size_t base_smem(int nv, int T, int S, int G, int NT) {
 }
 
 // the one-CTA-per-row big-row layout (micro_phase_bigc): 32 xi planes of
-// nvy nvz columns, a multiple of 256 (two threads per column at 512 threads),
-// mirrored grid with xi constant on each plane
+// nvy nvz = 256 columns, mirrored grid with xi constant on each plane
 static bool bigc_layout(const MeshDev& m) {
-  return m.nvyz > 1 && m.nvyz % 256 == 0 && m.nv / m.nvyz == BIGC_NXI && m.mirror && m.xplane;
+  return m.nvyz == BIGC_S && m.nv == BIGC_S * BIGC_NXI && m.mirror && m.xplane;
 }
 
 static size_t local_smem(int nx, int adaptation) {
@@ -2408,7 +2422,7 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   static const bool no_bigc = getenv("PK_NO_BIGC") != nullptr;
   const size_t rowbufs = ((size_t)3 * a.m.nv + a.m.nv / a.m.nvyz + 1) / 2 * 16 + 16;
   const size_t scr = (NT / 32) * (size_t)BIG_SCR * 8;  // (T < 0) plan scratch, aliased under bigc
-  a.bigc = T < 0 && NT == 512 && !no_bigc && bigc_layout(a.m) &&
+  a.bigc = T < 0 && NT == 256 && !no_bigc && bigc_layout(a.m) &&
            base_smem(a.m.nv, T, S, G, NT) - scr + rowbufs + 16 * 8 <= 226 * 1024 &&
            (size_t)(NT / 32) * BIG_SCR <= 2 * (size_t)a.m.nv;
   const size_t base = base_smem(a.m.nv, T, S, G, NT) + (a.bigc ? rowbufs - scr : 0);
@@ -2604,7 +2618,6 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   if (a.m.nvyz > 1) {  // 1D-3V rows: generic layout up to 256 nodes, big rows beyond
     if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
-    if (bigc_layout(a.m) && !getenv("PK_NO_BIGC")) return launch_T<-1, 1, 0, 512>(a, C, st);
     return launch_T<-1, 1, 0, 256>(a, C, st);
   }
   if ((a.m.nv == 64 || a.m.nv == 128) && !a.m.mirror)  // G8 needs the mirrored grid

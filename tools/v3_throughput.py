@@ -63,9 +63,6 @@ def main():
         ns = max(int(c[5]), 1)
         print("   slice0 cycles/step: micro %d, bar %d, finish %d, prepare %d, bar %d"
               % tuple(int(x) // ns for x in c[:5]))
-        nr = max(int(c[29]), 1)
-        print("   bigc row (CTA 0 of slice 0), cycles/row: wait %d, compute %d, sync %d, "
-              "writeback %d, moments %d over %d rows" % (*(int(x) // nr for x in c[24:29]), nr))
         print("   launch (CTAs per cluster, slices per cluster, on chip, group/bigc):",
               ens.dev.last_launch())
 
