@@ -193,6 +193,7 @@ def main():
     ap.add_argument("--impl", default="b200")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parareal", action="store_true")
+    ap.add_argument("--no-v3", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -301,6 +302,8 @@ def main():
         par = parareal_cfg2(barrier, maxr)
         if rank == 0:
             extra["parareal"] = par
+    if rank == 0 and not args.no_v3:
+        extra["v3"] = v3_default_grid(peak)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "fine_kernel_traffic.json")
     if os.path.exists(tpath):
@@ -374,6 +377,53 @@ def parareal_cfg2(barrier, maxr):
             "fine_cell_updates": fine_updates,
             "fine_cell_updates_per_s": fine_updates / max(tm.fine_total, 1e-12),
             "reference_cpu_s_build_container_1core": 41.7}
+
+
+def v3_default_grid(peak, nx=128, B=37, steps=20):
+    """The reference's own 1D-3V default velocity grid (32 x 16 x 16 nodes per
+    interface), B seeded-recipe instances of nx cells through the ensemble API,
+    all-kinetic steps at the reference stable dt: device-resident fine
+    throughput (CUDA events around one launch of `steps` steps, after a
+    warm-up launch) and its fraction of the HBM roofline at 16 B per update."""
+    import numpy as np
+    import torch
+
+    import paper_2511_13386_b200 as pk
+    from paper_2511_13386_b200.ensemble import Ensemble
+
+    m = pk.build_mesh(pk.MeshSpec(nx=nx, nvx=32, nvy=16, nvz=16))
+    grid = m.vgrid
+    w = grid.xi**4 * grid.M
+
+    def f(x):
+        return w[None] * (1.0 + 0.9 * np.cos(2.0 * np.pi * x / m.x_star))[:, None, None, None]
+
+    rho = m.bracket_x(f(m.x_centers))
+    f_if = f(m.x_interfaces)
+    g0 = f_if - m.bracket_x(f_if)[:, None, None, None] * grid.M[None]
+    rb = float(rho.sum() * m.dx / m.x_star)
+    E0 = pk.solve_field(rho, rb, m)
+    p = pk.KineticStepParams.default(m, 0.5, e_max=float(np.abs(E0).max()))
+    ens = Ensemble(m, [0.5] * B, [p.dt] * B, [rb] * B)
+    rho_d = torch.from_numpy(np.tile(rho, (B, 1))).cuda()
+    g_d = torch.from_numpy(np.tile(g0.reshape(1, nx, -1), (B, 1, 1))).cuda()
+    ms = None
+    for _ in range(2):
+        ens.load(rho_d, g_d)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ens.run(steps)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    upd = B * steps * nx * m.nv
+    val = upd / (ms * 1e-3)
+    C, K, on_chip, layout = ens.dev.last_launch()
+    return {"config": f"1D-3V default grid: {B} instances x Nx={nx} x (32x16x16) velocity nodes, "
+                      f"{steps} kinetic steps, eps=0.5, device-resident",
+            "value": val, "unit": "cell-updates/s", "ms": ms,
+            "roofline_frac": val * 16 / (peak * 1e9),
+            "layout": "one CTA per row" if layout == 2 else "warp per row"}
 
 
 if __name__ == "__main__":

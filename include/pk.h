@@ -109,7 +109,8 @@ int32_t pk_debug_profile(pk_ctx* ctx, void* dev_counters);
  * laid out: out[0] CTAs per thread-block cluster (or software group), out[1]
  * slices per cluster, out[2] 1 when the slice vectors were kept in shared
  * memory, out[3] 1 when the group was a software group (cooperative launch,
- * moments through global memory) rather than a hardware cluster. */
+ * moments through global memory) rather than a hardware cluster, 2 when big
+ * 1D-3V rows ran one CTA per row. */
 int32_t pk_fine_last_launch(pk_ctx* ctx, int32_t out[4]);
 
 /* --- fine propagator F --------------------------------------------------

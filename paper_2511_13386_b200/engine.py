@@ -223,11 +223,12 @@ class Device:
             raise_for(code, f"{what}: {msg.decode() if msg else ''}")
 
     def last_launch(self):
-        """Layout of this thread's last fine launch: (CTAs per cluster,
-        slices per cluster, slice vectors in shared memory, software group)."""
+        """Layout of this thread's last fine launch: (CTAs per cluster or group,
+        slices per cluster, slice vectors in shared memory, kind: 0 hardware
+        cluster, 1 software group, 2 big rows one CTA per row)."""
         out = (C.c_int32 * 4)()
         self._rc(self.lib.pk_fine_last_launch(self.ctx, out), "pk_fine_last_launch")
-        return out[0], out[1], bool(out[2]), bool(out[3])
+        return out[0], out[1], bool(out[2]), int(out[3])
 
     def check_stream(self, stream):
         """Raise this context's latched status after the work queued on

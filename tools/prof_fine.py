@@ -61,7 +61,7 @@ def main():
               % tuple(int(x) // ns for x in c[8:14]))
         print("   slice vectors in shared memory:", bool(c[15]))
         C, K, _, sg = ens.dev.last_launch()
-        print(f"   launch: {'software groups' if sg else 'clusters'} of {C} CTAs x {K} slices")
+        print(f"   launch: {'software groups' if sg == 1 else 'clusters'} of {C} CTAs x {K} slices")
         if a.per_cta:
             ncta = (a.B + K - 1) // K * C
             pc = c[32:32 + 3 * ncta].reshape(ncta, 3)
