@@ -1568,9 +1568,7 @@ __device__ void micro_phase_big(const FineArgs& a, const SliceView& v, const Sme
 
 // Big rows, one CTA per row (FineArgs::bigc): the reference's default 1D-3V
 // grid, 32 xi planes of nvy nvz = 256 (vy, vz) columns, mirrored, xi constant
-// on each plane.  The CTA's rows stream through two shared-memory row buffers
-// filled by single TMA bulk copies, the next row landing while the current
-// one is worked on; M and the per-plane xi sit in shared memory.
+// on each plane.
 //
 // The thread layout follows the row moments.  <q> folds plane jx with plane
 // 31-jx and sums the 4096 folded terms pairwise (mesh.py:95-133): 32 leaves
@@ -1579,24 +1577,38 @@ __device__ void micro_phase_big(const FineArgs& a, const SliceView& v, const Sme
 // a butterfly, then a perfectly balanced tree over the leaves.  Thread (l, k)
 // -- warp l / 4, lanes 8 (l % 4) + k -- updates exactly the nodes of its
 // accumulator: columns 128 (l % 2) + k + 8 m of planes jx and 31 - jx (xi < 0
-// and its mirror xi > 0), 32 nodes, and accumulates its fold terms in
-// registers in leaf order; the leaf butterfly is group_leaf's (shuffles in
-// the 8-lane group), the tree a 32-lane butterfly of warp 0 over the leaves
-// in order.  One barrier per row.  Node updates: the operations of
-// big_micro_row (kinetic.py:148-224) in its order, the xi neighbours c -/+ S
-// from the staged row, the x neighbour (row i+1 for xi < 0, i-1 for xi > 0)
-// from L2, the zero upwind term skipped as in the fast layouts (equal up to
-// the sign of zero).
+// and its mirror xi > 0), 32 nodes (their M in registers), and accumulates
+// its fold terms in registers in leaf order; the leaf butterfly is
+// group_leaf's (shuffles in the 8-lane group), the tree a 32-lane butterfly
+// of warp 0 over the leaves in order.  One barrier per row.  Node updates:
+// the operations of big_micro_row (kinetic.py:148-224) in its order, the
+// zero upwind term skipped as in the fast layouts (equal up to the sign of
+// zero).
+//
+// Staging.  Dense phases (every row kinetic, rows p0..p1-1 in order): the
+// lower halves (planes 0-15) of rows p0..p1 and the upper halves (planes
+// 16-31) of rows p0-1..p1-1 stream through three 32 KB shared-memory slots
+// each, one TMA bulk copy per half, issued two rows ahead; row i then reads
+// its own halves, the lower half of row i+1 (x neighbour for xi < 0) and the
+// upper half of row i-1 (for xi > 0) from shared memory -- no global loads in
+// the node loop.  Sparse phases (listed rows, hybrid): two full-row slots,
+// the next listed row landing while the current one is worked on, the x
+// neighbour from L2.
 constexpr int BIGC_NXI = 32;   // xi planes
 constexpr int BIGC_S = 256;    // (vy, vz) columns per plane
 
+// running fill counters of the staging mbarriers: [0] full-row slots
+// (mbar 0-1), [1] lower-half slots (mbar 2-4), [2] upper-half slots (mbar 5-7)
+struct BigcCnt {
+  uint32_t q[3];
+};
+
 __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                  const double* gin, double* gout, int crank, int C, double* rbuf,
-                                 const double* sM, const double* sxi, uint64_t* mbar,
-                                 uint32_t& qbase) {
-  constexpr int S = BIGC_S, X = BIGC_NXI, NM = 16;
+                                 const double* sxi, uint64_t* mbar, BigcCnt& cnt) {
+  constexpr int S = BIGC_S, X = BIGC_NXI, NM = 16, HX = X / 2;
   const MeshDev& m = a.m;
-  const int nx = m.nx, nv = m.nv;
+  const int nx = m.nx, nv = m.nv, hv = nv / 2;
   const int nk = __ldcg(v.nk);
   const bool dense = nk == nx;
   const int p0 = (int)(((long long)crank * nk) / C), p1 = (int)(((long long)(crank + 1) * nk) / C);
@@ -1609,6 +1621,13 @@ __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Sm
   const int col0 = (l & 1) * 128 + k;
   const bool sq = a.adaptation != 0;
   const double xl = sxi[jx], xh = sxi[jm];
+  const double dx = m.dx, rdx = m.rdx;
+  double Ml[NM], Mh[NM];
+#pragma unroll
+  for (int u = 0; u < NM; ++u) {
+    Ml[u] = __ldg(m.M + jx * S + col0 + 8 * u);
+    Mh[u] = __ldg(m.M + jm * S + col0 + 8 * u);
+  }
   auto rowid = [&](int p) { return dense ? p : __ldcg(v.klist + p); };
   auto coef = [&](int i) {
     RowCoef rc;
@@ -1620,82 +1639,50 @@ __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Sm
     rc.k2 = P.k2[o + i];
     return rc;
   };
-  const uint32_t bytes = (uint32_t)nv * 8;
-  // row q of this phase goes to slot (qbase + q) & 1 at parity ((qbase + q) >> 1) & 1
-  auto issue = [&](int q, int i) {
-    if (tid == 0) {
-      const uint32_t Q = qbase + (uint32_t)q;
-      mbar_expect_tx(mbar + (Q & 1), bytes);
-      bulk_g2s(rbuf + (size_t)(Q & 1) * nv, gin + (size_t)i * nv, bytes, mbar + (Q & 1));
-    }
+  // one bulk copy of `bytes` from src into slot `dst`, completing mbarrier mb
+  auto copy = [&](double* dst, const double* src, uint32_t bytes, uint64_t* mb) {
+    mbar_expect_tx(mb, bytes);
+    bulk_g2s(dst, src, bytes, mb);
   };
-  if (tid == 0) fence_proxy_async_global();  // rows written by the generic proxy, read by TMA
-  int i_cur = rowid(p0);
-  issue(0, i_cur);
-  int i_nxt = p0 + 1 < p1 ? rowid(p0 + 1) : 0;
-  if (p0 + 1 < p1) issue(1, i_nxt);
-  RowCoef rc = coef(i_cur);
-  const double dx = m.dx, rdx = m.rdx;
-  for (int p = p0; p < p1; ++p) {
-    const int q = p - p0;
-    const uint32_t Q = qbase + (uint32_t)q;
-    const double* rb = rbuf + (size_t)(Q & 1) * nv;
-    const int i = i_cur;
-    // next row's id and coefficients ride ahead of the current row's work
-    const int i_n2 = p + 2 < p1 ? rowid(p + 2) : 0;
-    RowCoef rn = rc;
-    if (p + 1 < p1) rn = coef(i_nxt);
+  // The node update of plane jx (lower, xi < 0) and jm (upper, xi > 0) for
+  // u = 0..15: g/gb/gf the node and its xi neighbours, xn the x neighbour.
+  // Leaves the outputs in yl/yh and the fold-term accumulators in a1/a2.
+  auto row_update = [&](const RowCoef& rc, auto lo_at, auto hi_at, double (&yl)[NM],
+                        double (&yh)[NM], double& a1, double& a2) {
     const double Ep = rc.vsg > 0 ? rc.vco : 0.0;
     const double Em = rc.vsg < 0 ? rc.vco : 0.0;
-    // x neighbours from L2 first (row i+1 on the lower plane, i-1 on the upper)
-    const double* gnl = gin + (size_t)wrap(i + 1, nx) * nv + jx * S + col0;
-    const double* gph = gin + (size_t)wrap(i - 1, nx) * nv + jm * S + col0;
-    double xa[NM], xb[NM];
 #pragma unroll
     for (int u = 0; u < NM; ++u) {
-      xa[u] = __ldcg(gnl + 8 * u);
-      xb[u] = __ldcg(gph + 8 * u);
-    }
-    mbar_wait(mbar + (Q & 1), (Q >> 1) & 1);
-    const double* rl = rb + jx * S + col0;
-    const double* rh = rb + jm * S + col0;
-    const double* Ml = sM + jx * S + col0;
-    const double* Mh = sM + jm * S + col0;
-    double a1 = 0.0, a2 = 0.0;
-#pragma unroll
-    for (int u = 0; u < NM; ++u) {
-      const int c = 8 * u;
+      double g, gb, gf, xn;
+      lo_at(u, g, gb, gf, xn);
       double lo, hi;
       {  // plane jx, xi < 0: x-upwind from row i+1; zero xi-inflow below plane 0
-        const double g = rl[c];
-        double w = xl * (xa[u] - g);
+        double w = xl * (xn - g);
         w = qdiv(w, dx, rdx);
-        const double gb = rl[c - S];  // (jx = 0: before the row, inside shared memory, unused)
         const double dm = jx == 0 ? g : g - gb;
         w = w + dm * Ep;
-        const double dp = rl[c + S] - g;  // (jx + 1 <= 16 < X)
+        const double dp = gf - g;  // (jx + 1 <= 16 < X)
         w = w + dp * Em;
-        const double Mc = Ml[c];
+        const double Mc = Ml[u];
         w = w - Mc * rc.dc;
         const double forcing = w + (xl * Mc) * rc.J;
         lo = rc.k1 * g - rc.k2 * forcing;
       }
+      hi_at(u, g, gb, gf, xn);
       {  // plane 31 - jx, xi > 0: x-upwind from row i-1; zero inflow above plane 31
-        const double g = rh[c];
-        double w = xh * (g - xb[u]);
+        double w = xh * (g - xn);
         w = qdiv(w, dx, rdx);
-        const double dm = g - rh[c - S];  // (jm - 1 >= 15 >= 0)
+        const double dm = g - gb;  // (jm - 1 >= 15 >= 0)
         w = w + dm * Ep;
-        const double gq = rh[c + S];  // (jm = 31: past the row, inside shared memory, unused)
-        const double dp = jm + 1 == X ? -g : gq - g;
+        const double dp = jm + 1 == X ? -g : gf - g;
         w = w + dp * Em;
-        const double Mc = Mh[c];
+        const double Mc = Mh[u];
         w = w - Mc * rc.dc;
         const double forcing = w + (xh * Mc) * rc.J;
         hi = rc.k1 * g - rc.k2 * forcing;
       }
-      xa[u] = lo;
-      xb[u] = hi;
+      yl[u] = lo;
+      yh[u] = hi;
       // fold terms (q(j) + q(mirror j)), accumulated in leaf order
       const double f1 = xl * lo + xh * hi;
       a1 = u == 0 ? f1 : a1 + f1;
@@ -1704,14 +1691,17 @@ __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Sm
         a2 = u == 0 ? f2 : a2 + f2;
       }
     }
+  };
+  // stores, leaf butterflies, the tree over the leaves and the moments of row i
+  auto row_finish = [&](int i, const double (&yl)[NM], const double (&yh)[NM], double a1,
+                        double a2) {
     double* ol = gout + (size_t)i * nv + jx * S + col0;
     double* oh = gout + (size_t)i * nv + jm * S + col0;
 #pragma unroll
     for (int u = 0; u < NM; ++u) {
-      __stcg(ol + 8 * u, xa[u]);
-      __stcg(oh + 8 * u, xb[u]);
+      __stcg(ol + 8 * u, yl[u]);
+      __stcg(oh + 8 * u, yh[u]);
     }
-    // leaf: group_leaf's butterfly over the eight accumulators
     a1 = a1 + __shfl_xor_sync(FULL, a1, 1);
     a1 = a1 + __shfl_xor_sync(FULL, a1, 2);
     a1 = a1 + __shfl_xor_sync(FULL, a1, 4);
@@ -1724,7 +1714,7 @@ __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Sm
       sm.red[l] = a1;
       sm.red[32 + l] = a2;
     }
-    __syncthreads();  // leaves ready; every thread is done with the staged row
+    __syncthreads();  // leaves ready; every thread is done with the staged data
     if (tid < 32) {   // balanced tree over the 32 leaves in order
       double r1 = sm.red[lane], r2 = sm.red[32 + lane];
 #pragma unroll
@@ -1738,6 +1728,136 @@ __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Sm
       }
       __syncwarp();
     }
+  };
+  if (tid == 0) fence_proxy_async_global();  // rows written by the generic proxy, read by TMA
+
+  if (dense) {
+    // lower halves L_t = row p0 + t (t = 0..n), upper halves U_t = row p0 - 1 + t
+    const int n = p1 - p0;
+    const uint32_t lb = cnt.q[1], ub = cnt.q[2];
+    double* const lslot = rbuf;           // 3 lower-half slots
+    double* const uslot = rbuf + 3 * hv;  // 3 upper-half slots
+    auto issue_l = [&](int t) {
+      const uint32_t T = lb + (uint32_t)t;
+      copy(lslot + (T % 3) * hv, gin + (size_t)wrap(p0 + t, nx) * nv, hv * 8, mbar + 2 + T % 3);
+    };
+    auto issue_u = [&](int t) {
+      const uint32_t T = ub + (uint32_t)t;
+      copy(uslot + (T % 3) * hv, gin + (size_t)wrap(p0 - 1 + t, nx) * nv + hv, hv * 8,
+           mbar + 5 + T % 3);
+    };
+    auto wait_l = [&](int t) {
+      const uint32_t T = lb + (uint32_t)t;
+      mbar_wait(mbar + 2 + T % 3, (T / 3) & 1);
+      return lslot + (T % 3) * hv;
+    };
+    auto wait_u = [&](int t) {
+      const uint32_t T = ub + (uint32_t)t;
+      mbar_wait(mbar + 5 + T % 3, (T / 3) & 1);
+      return uslot + (T % 3) * hv;
+    };
+    if (tid == 0)
+      for (int t = 0; t < 3 && t <= n; ++t) {
+        issue_l(t);
+        issue_u(t);
+      }
+    RowCoef rc = coef(p0);
+    for (int q = 0; q < n; ++q) {
+      const int i = p0 + q;
+      RowCoef rn = rc;
+      if (q + 1 < n) rn = coef(i + 1);
+      const double* Lc = wait_l(q);      // own lower half
+      const double* Ln = wait_l(q + 1);  // row i+1, lower half
+      const double* Up = wait_u(q);      // row i-1, upper half
+      const double* Uc = wait_u(q + 1);  // own upper half
+      const double* rl = Lc + jx * S + col0;
+      const double* rlf = jx + 1 < HX ? rl + S : Uc + col0;  // plane jx + 1
+      const double* xl_ = Ln + jx * S + col0;
+      const double* rh = Uc + (jm - HX) * S + col0;
+      const double* rhb = jm > HX ? rh - S : Lc + (HX - 1) * S + col0;  // plane jm - 1
+      const double* xh_ = Up + (jm - HX) * S + col0;
+      double yl[NM], yh[NM], a1 = 0.0, a2 = 0.0;
+      row_update(
+          rc,
+          [&](int u, double& g, double& gb, double& gf, double& xn) {
+            g = rl[8 * u];
+            gb = jx > 0 ? rl[8 * u - S] : 0.0;
+            gf = rlf[8 * u];
+            xn = xl_[8 * u];
+          },
+          [&](int u, double& g, double& gb, double& gf, double& xn) {
+            g = rh[8 * u];
+            gb = rhb[8 * u];
+            gf = jm + 1 < X ? rh[8 * u + S] : 0.0;
+            xn = xh_[8 * u];
+          },
+          yl, yh, a1, a2);
+      row_finish(i, yl, yh, a1, a2);
+      // (after row_finish's barrier) slots of L_q and U_q are free: L_{q+3}, U_{q+3}
+      if (tid == 0) {
+        if (q + 3 <= n) issue_l(q + 3);
+        if (q + 3 <= n) issue_u(q + 3);
+      }
+      rc = rn;
+    }
+    cnt.q[1] += (uint32_t)(n + 1);
+    cnt.q[2] += (uint32_t)(n + 1);
+    return;
+  }
+
+  // sparse: two full-row slots, the x neighbours from L2
+  uint32_t& qbase = cnt.q[0];
+  const uint32_t bytes = (uint32_t)nv * 8;
+  // row q of this phase goes to slot (qbase + q) & 1 at parity ((qbase + q) >> 1) & 1
+  auto issue = [&](int q, int i) {
+    if (tid == 0) {
+      const uint32_t Q = qbase + (uint32_t)q;
+      copy(rbuf + (size_t)(Q & 1) * nv, gin + (size_t)i * nv, bytes, mbar + (Q & 1));
+    }
+  };
+  int i_cur = rowid(p0);
+  issue(0, i_cur);
+  int i_nxt = p0 + 1 < p1 ? rowid(p0 + 1) : 0;
+  if (p0 + 1 < p1) issue(1, i_nxt);
+  RowCoef rc = coef(i_cur);
+  for (int p = p0; p < p1; ++p) {
+    const int q = p - p0;
+    const uint32_t Q = qbase + (uint32_t)q;
+    const double* rb = rbuf + (size_t)(Q & 1) * nv;
+    const int i = i_cur;
+    // next row's id and coefficients ride ahead of the current row's work
+    const int i_n2 = p + 2 < p1 ? rowid(p + 2) : 0;
+    RowCoef rn = rc;
+    if (p + 1 < p1) rn = coef(i_nxt);
+    // x neighbours from L2 first (row i+1 on the lower plane, i-1 on the upper)
+    const double* gnl = gin + (size_t)wrap(i + 1, nx) * nv + jx * S + col0;
+    const double* gph = gin + (size_t)wrap(i - 1, nx) * nv + jm * S + col0;
+    double xa[NM], xb[NM];
+#pragma unroll
+    for (int u = 0; u < NM; ++u) {
+      xa[u] = __ldcg(gnl + 8 * u);
+      xb[u] = __ldcg(gph + 8 * u);
+    }
+    mbar_wait(mbar + (Q & 1), (Q >> 1) & 1);
+    const double* rl = rb + jx * S + col0;
+    const double* rh = rb + jm * S + col0;
+    double yl[NM], yh[NM], a1 = 0.0, a2 = 0.0;
+    row_update(
+        rc,
+        [&](int u, double& g, double& gb, double& gf, double& xn) {
+          g = rl[8 * u];
+          gb = jx > 0 ? rl[8 * u - S] : 0.0;
+          gf = rl[8 * u + S];
+          xn = xa[u];
+        },
+        [&](int u, double& g, double& gb, double& gf, double& xn) {
+          g = rh[8 * u];
+          gb = rh[8 * u - S];
+          gf = jm + 1 < X ? rh[8 * u + S] : 0.0;
+          xn = xb[u];
+        },
+        yl, yh, a1, a2);
+    row_finish(i, yl, yh, a1, a2);
     if (p + 2 < p1) issue(q + 2, i_n2);  // (the staged row was only read: no proxy fence)
     i_cur = i_nxt;
     i_nxt = i_n2;
@@ -1992,9 +2112,9 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
     if (T == 0) p += (size_t)nwpc * nv * 8;       // generic-layout row scratch
     if (T < 0 && !a.bigc) p += (size_t)nwpc * BIG_SCR * 8;   // big rows: plan scratch
     if (T < 0 && a.bigc) {
-      // big rows, one CTA per row: 2 row buffers, M, xi per plane; the plan
-      // scratch of the per-warp row operations (prologue, lifts: never during
-      // a micro phase) lives in the row buffers
+      // big rows, one CTA per row: row staging (six half-row or two full-row
+      // slots), xi per plane; the plan scratch of the per-warp row operations
+      // (prologue, lifts: never during a micro phase) lives in the staging
       p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
       ring = reinterpret_cast<double*>(p);
       sm.wrow = ring;
@@ -2021,8 +2141,7 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
       }
     if (T > 0 && threadIdx.x < (G < 0 ? 2 * S : nwpc * S)) mbar_init(mbar + threadIdx.x, 1);
     if (T < 0 && a.bigc) {
-      if (threadIdx.x < 2) mbar_init(mbar + threadIdx.x, 1);
-      for (int j = threadIdx.x; j < nv; j += blockDim.x) ring[2 * (size_t)nv + j] = m.M[j];
+      if (threadIdx.x < 8) mbar_init(mbar + threadIdx.x, 1);
       for (int j = threadIdx.x; j < nv / m.nvyz; j += blockDim.x)
         ring[3 * (size_t)nv + j] = m.vx[(size_t)j * m.nvyz];
     }
@@ -2089,6 +2208,7 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
   int* abort_flag = v.abort_;
   const size_t o = (size_t)b * nx;
   uint32_t qbase = 0, obase = 0;
+  BigcCnt bcnt = {{0u, 0u, 0u}};
   GSConsts<G < 0 ? -G : 1> gsc;
   if constexpr (G < 0) gsc.load(sm, threadIdx.x & 31);
   double* ring_w = ring ? ring + (size_t)(G < 0 ? 0 : warp) * S * RSN : nullptr;
@@ -2209,8 +2329,8 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
     else if constexpr (T == 0)
       micro_phase_gen(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     else if (a.bigc)
-      micro_phase_bigc(a, v, sm, ph, buf(s), buf(s + 1), crank, C, ring, ring + 2 * (size_t)nv,
-                       ring + 3 * (size_t)nv, mbar, qbase);
+      micro_phase_bigc(a, v, sm, ph, buf(s), buf(s + 1), crank, C, ring, ring + 3 * (size_t)nv,
+                       mbar, bcnt);
     else
       micro_phase_big(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     if (prof) { c1 = clock64(); tp[0] += c1 - c0; c0 = c1; }
