@@ -70,7 +70,15 @@ __device__ __forceinline__ double group_leaf(F x, int off, int n, bool act) {
   double r = 0.0, seq = -0.0;
   int full = 0;
   if (act) {
-    if (n < 8) {
+    if (n == 128) {  // full leaf: the 16 operands load back to back, then the chain
+      full = 128;
+      double t[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) t[j] = x(off + 8 * j + k);
+      r = t[0];
+#pragma unroll
+      for (int j = 1; j < 16; ++j) r = r + t[j];
+    } else if (n < 8) {
       for (int i = 0; i < n; ++i) seq = seq + x(off + i);
     } else {
       full = n - (n % 8);
