@@ -1008,6 +1008,9 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
                                uint64_t* mbar, uint32_t& qbase) {
   constexpr int NV = 16 * CH;
   constexpr int RS = NV + 8;  // ring row stride in doubles (64 B pad)
+  // an operation holds rows p-1 .. p+4 of the stream at once: a shallower
+  // ring would wait forever for a slot it has not released
+  static_assert(S >= 6, "G8 ring needs >= 6 slots per warp");
   const MeshDev& m = a.m;
   const int nx = m.nx;
   const int lane = threadIdx.x & 31;
