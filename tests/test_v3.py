@@ -97,3 +97,31 @@ def test_v3_parareal_golden(gold):
     assert np.array_equal(np.stack(res.ledger.rho), d["p_rows"])
     assert np.array_equal(res.ledger.err, d["p_err"])
     assert [res.iterations, res.status == "converged"] == list(d["p_meta"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("eps,thr", [(1e-2, 1e-2), (1e-2, 1e-3), (1e-3, 1e-3)])
+def test_v3_default_grid_mixed_labels_golden(gold, eps, thr):
+    """The reference's default velocity grid (32 x 16 x 16) on partly kinetic
+    slices (tests/golden/make_3v_mixed_golden.py): labels mixed at 38 % / 94 %
+    or shrinking to all-fluid, so the one-CTA-per-row layout runs its sparse
+    (listed-row) phases and the kinetic -> fluid zeroing; bitwise."""
+    from paper_2511_13386_b200.engine import Device
+
+    d = gold("v3_mixed")
+    k = f"{eps:g}_{thr:g}"
+    m = mesh((32, 32, 16, 16))
+    rho, _, rb = initial(m)
+    E0 = pk.solve_field(rho, rb, m)
+    p = pk.KineticStepParams.default(m, eps, e_max=float(np.abs(E0).max()))
+    assert p.dt == d[k + "_dt"]
+    gs = pk.lift(rho, E0, eps, m, order=2, rho_bar=rb).g
+    st = pk.HybridState.initial(pk.MacroState(rho, E0, 0.0), pk.MicroState(gs), m)
+    res = pk.hybrid_propagate(st, 12.5 * p.dt, p, pk.Thresholds(thr, thr), pk.HybridOptions(), m,
+                              rb, field_rtol=1.0)
+    assert Device.for_mesh(m).last_launch()[3] == 2  # one CTA per row
+    assert np.array_equal(res.labels.kinetic_cells, d[k + "_kc"])
+    assert np.array_equal(res.labels.kinetic_ifaces, d[k + "_ki"])
+    assert np.array_equal(res.macro.rho, d[k + "_rho"]) and np.array_equal(res.macro.E, d[k + "_E"])
+    assert np.array_equal(res.E_prev, d[k + "_Ep"])
+    assert digest(res.micro.g) == str(d[k + "_g"])
