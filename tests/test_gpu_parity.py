@@ -357,6 +357,53 @@ def test_packed_clusters_match_one_slice_per_cluster(nv, B, sg):
         assert eq(outs[0][0][b], r) and eq(outs[0][1][b], EE) and eq(outs[0][2][b], gg)
 
 
+def test_software_groups_nonfinite_and_mid_run_trips():
+    """Software groups (256 all-kinetic slices, 7 per group of 8 CTAs) with
+    slices that go non-finite (dt far past the stable one: the moments become
+    quiet NaNs, which the owner's sentinel poll must accept) and, under a
+    tight field guard, slices that trip it at some step: every slice -- the
+    blown-up and the aborted ones included -- must come out bitwise as with one
+    slice per single-CTA cluster."""
+    import torch
+
+    from paper_2511_13386_b200.engine import Device, HybridKnobs, make_phase
+
+    B, nx, nv = 256, 256, 128
+    cases = configs.cfg5(range(B), nx=nx, nv=nv)
+    m = cases[0].mesh
+    dev = Device.for_mesh(m)
+    grid = O.make_grid(nx, nv)
+    eps = [c.eps for c in cases]
+    dts = [O.stable_dt(grid, c.eps, e_max=float(np.abs(O.field(c.rho, c.rho_bar, grid)).max()))
+           for c in cases]
+    for b in (3, 100, 200):
+        dts[b] *= 1e3
+    nst = [12] * B
+    ph = [make_phase(m, eps, dts, nst), make_phase(m, eps, dts, [0] * B)]
+    outs = []
+    for hint in (0, 1):
+        rho = dev.t(np.stack([c.rho for c in cases]))
+        g = dev.t(np.stack([c.g.reshape(nx, nv) for c in cases]))
+        E = torch.zeros_like(rho)
+        Ep = torch.zeros_like(rho)
+        kc = torch.ones((B, nx), dtype=torch.uint8, device=dev.device)
+        ki = torch.ones_like(kc)
+        dev.fine(rho, E, Ep, kc, ki, g, dev.t(np.array([c.rho_bar for c in cases])), [0] * B,
+                 ph, HybridKnobs(), eps, 1e-14, cluster_hint=hint)
+        try:
+            dev.check()
+            tripped = False
+        except pk.SolvabilityViolation:
+            tripped = True
+        Cc, K, _, soft = dev.last_launch()
+        assert (soft == 1) if hint == 0 else (Cc, K, soft) == (1, 1, 0)
+        outs.append([tripped] + [x.cpu().numpy() for x in (rho, E, g)])
+    assert outs[0][0] == outs[1][0]
+    for x0, x1 in zip(outs[0][1:], outs[1][1:]):
+        assert np.array_equal(x0, x1, equal_nan=True)
+    assert not np.isfinite(outs[0][3][100]).all()  # (the blown-up slice)
+
+
 def test_eps_profile_hybrid_vs_oracle():
     """eps(x) extension (cfg3 profile) on a reduced grid: device == oracle restatement."""
     nx, nv = 64, 64
