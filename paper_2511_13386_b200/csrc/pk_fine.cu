@@ -1105,6 +1105,14 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
     return s_ring + slot * (RS * 8);
   };
 
+  // this lane's column constants (columns k + 8 mm and their mirrors) stay in
+  // registers for the whole phase
+  double vxr[CH], Mr[CH];
+#pragma unroll
+  for (int mm = 0; mm < CH; ++mm) {
+    vxr[mm] = lds64(s_vx + 8 * (k + 8 * mm));
+    Mr[mm] = lds64(s_M + 8 * (k + 8 * mm));
+  }
   pump(S);
   // per-row coefficients, one row per lane, 32 rows per batch
   struct Coef {
@@ -1205,8 +1213,8 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
         // mirrored grid (m.mirror): vx[u] = -vx[c], M[u] = M[c], and xiM is
         // vx * M as the host formed it, so one column's constants serve both
         // halves and xiM costs a multiply instead of a shared-memory load
-        const double vxc = lds64(s_vx + 8 * c), vxu = -vxc;
-        const double Mc = lds64(s_M + 8 * c);
+        const double vxc = vxr[mm], vxu = -vxc;
+        const double Mc = Mr[mm];
         const double xMc = vxc * Mc, xMu = -xMc;
         double lo, hi;
         {  // lower half, xi < 0: x-upwind from row i+1; zero inflow at -v*
