@@ -1,6 +1,8 @@
 """Device (libpk) vs oracle / golden vectors.  Exact mode: bitwise equality
 (np.array_equal, i.e. equal up to the sign of zero)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -343,7 +345,8 @@ def test_packed_clusters_match_one_slice_per_cluster(nv, B, sg):
         Cc, K, on_chip, soft = dev.last_launch()
         assert on_chip
         if hint == 0:
-            assert 1 < K < Cc and (sg is None or (soft == 1) == sg), (Cc, K, soft)
+            if not os.environ.get("PK_NO_SG"):  # (the A/B switch turns software groups off)
+                assert 1 < K < Cc and (sg is None or (soft == 1) == sg), (Cc, K, soft)
         else:
             assert (Cc, K, soft) == (1, 1, 0)
         outs.append([x.cpu().numpy() for x in (rho, E, g)])
@@ -396,7 +399,10 @@ def test_software_groups_nonfinite_and_mid_run_trips():
         except pk.SolvabilityViolation:
             tripped = True
         Cc, K, _, soft = dev.last_launch()
-        assert (soft == 1) if hint == 0 else (Cc, K, soft) == (1, 1, 0)
+        if hint == 1:
+            assert (Cc, K, soft) == (1, 1, 0)
+        elif not os.environ.get("PK_NO_SG"):
+            assert soft == 1
         outs.append([tripped] + [x.cpu().numpy() for x in (rho, E, g)])
     assert outs[0][0] == outs[1][0]
     for x0, x1 in zip(outs[0][1:], outs[1][1:]):

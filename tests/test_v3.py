@@ -3,6 +3,8 @@ vectors from the real reference (tests/golden/make_3v_golden.py): host mesh
 and brackets on CPU; kinetic steps, lift, hybrid steps with adaptation and a
 parareal run on the B200, bitwise."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -119,7 +121,8 @@ def test_v3_default_grid_mixed_labels_golden(gold, eps, thr):
     st = pk.HybridState.initial(pk.MacroState(rho, E0, 0.0), pk.MicroState(gs), m)
     res = pk.hybrid_propagate(st, 12.5 * p.dt, p, pk.Thresholds(thr, thr), pk.HybridOptions(), m,
                               rb, field_rtol=1.0)
-    assert Device.for_mesh(m).last_launch()[3] == 2  # one CTA per row
+    if not os.environ.get("PK_NO_BIGC"):  # (the A/B switch selects the warp layout)
+        assert Device.for_mesh(m).last_launch()[3] == 2  # one CTA per row
     assert np.array_equal(res.labels.kinetic_cells, d[k + "_kc"])
     assert np.array_equal(res.labels.kinetic_ifaces, d[k + "_ki"])
     assert np.array_equal(res.macro.rho, d[k + "_rho"]) and np.array_equal(res.macro.E, d[k + "_E"])
