@@ -253,7 +253,7 @@ pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   }
   cudaMemcpy(c->d_const, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(c->d_plan, plan, 3 * sizeof(PwPlan), cudaMemcpyHostToDevice);
-  cudaMemset(c->d_status, 0, sizeof(pk::Status));
+  cudaMemset(c->d_status, 0xFF, sizeof(pk::Status));
   m.vx = c->d_const;
   m.M = c->d_const + nv;
   m.xiM = c->d_const + 2 * nv;
@@ -281,6 +281,20 @@ int32_t pk_reserve(pk_ctx* c, int32_t max_slices) {
   return ensure(c, max_slices);
 }
 
+// pk_device.cuh Status key -> pk_status (all ones = no error)
+static void decode_status(const pk::Status& s, pk_status* out) {
+  if (s.key == ~0ull) {
+    out->code = 0;
+    out->slice = 0;
+    out->step = 0;
+  } else {
+    out->code = (int32_t)(s.key & 0xFF);
+    out->step = (int32_t)(uint32_t)((s.key >> 8) & 0xFFFFFFFFull);
+    out->slice = (int32_t)(s.key >> 40) - 1;
+  }
+  out->pad = 0;
+}
+
 int32_t pk_status_read_stream(pk_ctx* c, pk_status* out, int32_t clear, void* stream) {
   if (!c || !out) return PK_ERR_BAD_ARG;
   cudaSetDevice(c->device);
@@ -289,11 +303,8 @@ int32_t pk_status_read_stream(pk_ctx* c, pk_status* out, int32_t clear, void* st
   cudaError_t e = cudaMemcpyAsync(&s, c->d_status, sizeof(s), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(c, e, "status copy");
-  out->code = s.code;
-  out->slice = s.slice;
-  out->step = s.step;
-  out->pad = 0;
-  if (clear) cudaMemsetAsync(c->d_status, 0, sizeof(pk::Status), st);
+  decode_status(s, out);
+  if (clear) cudaMemsetAsync(c->d_status, 0xFF, sizeof(pk::Status), st);
   return PK_OK;
 }
 
@@ -305,11 +316,8 @@ int32_t pk_status_read(pk_ctx* c, pk_status* out, int32_t clear) {
   pk::Status s;
   e = cudaMemcpy(&s, c->d_status, sizeof(s), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(c, e, "status copy");
-  out->code = s.code;
-  out->slice = s.slice;
-  out->step = s.step;
-  out->pad = 0;
-  if (clear) cudaMemset(c->d_status, 0, sizeof(pk::Status));
+  decode_status(s, out);
+  if (clear) cudaMemset(c->d_status, 0xFF, sizeof(pk::Status));
   return PK_OK;
 }
 

@@ -310,19 +310,21 @@ __device__ __forceinline__ int wrap(int i, int n) {
   return i < 0 ? i + n : (i >= n ? i - n : i);
 }
 
-// Status record: first error wins.
+// Status record.  When several slices fail in one launch the LOWEST slice's
+// error is kept (atomicMin on slice+1 | step | code): the reference consumes
+// its window futures in window order, so `run` raises the lowest failing
+// window's error (parareal.py:260-266).  A slice stops at its first error, so
+// a slice never posts twice.  Empty record = all ones (pk_api.cu decodes it).
 struct Status {
-  int code;   // pk.h PK_ERR_*
-  int slice;
-  int step;
-  int pad;
+  unsigned long long key;   // (slice + 1) << 40 | (uint32)step << 8 | code
+  int pad0, pad1;
 };
 
 __device__ __forceinline__ void set_status(Status* st, int code, int slice, int step) {
-  if (atomicCAS(&st->code, 0, code) == 0) {
-    st->slice = slice;
-    st->step = step;
-  }
+  const unsigned long long key = ((unsigned long long)((unsigned)(slice + 1) & 0xFFFFFFu) << 40) |
+                                 ((unsigned long long)(unsigned)step << 8) |
+                                 (unsigned long long)(code & 0xFF);
+  atomicMin(&st->key, key);
 }
 
 }  // namespace pk

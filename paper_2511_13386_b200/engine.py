@@ -237,14 +237,14 @@ class Device:
         self._rc(self.lib.pk_status_read_stream(self.ctx, C.byref(st), 1,
                                                 C.c_void_p(stream.cuda_stream)), "status")
         if st.code:
-            raise_for(st.code, f"slice {st.slice}, step {st.step}")
+            raise_for(st.code, f"slice {st.slice}, step {st.step}", st.slice, st.step)
 
     def check(self):
         """Synchronise and raise the latched device status, if any."""
         st = _native.PkStatus()
         self._rc(self.lib.pk_status_read(self.ctx, C.byref(st), 1), "status")
         if st.code:
-            raise_for(st.code, f"slice {st.slice}, step {st.step}")
+            raise_for(st.code, f"slice {st.slice}, step {st.step}", st.slice, st.step)
 
     def reserve(self, B):
         self._rc(self.lib.pk_reserve(self.ctx, int(B)), "reserve")

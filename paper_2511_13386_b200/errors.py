@@ -56,9 +56,27 @@ _MESSAGES = {
 }
 
 
-def raise_for(code: int, detail: str = "") -> None:
+def raise_for(code: int, detail: str = "", slice=None, step=None) -> None:
+    """Raise the exception class of a libpk status code.  The raised object
+    carries ``pk_code`` and, for device-detected errors, the failing batch
+    entry ``pk_slice`` and ``pk_step`` (the parareal engine maps the slice to
+    its window)."""
     if code == 0:
         return
     cls = _BY_CODE.get(code, NativeError)
     msg = _MESSAGES.get(code, f"libpk error {code}")
-    raise cls(f"{msg}{': ' + detail if detail else ''}")
+    ex = cls(f"{msg}{': ' + detail if detail else ''}")
+    ex.pk_code, ex.pk_slice, ex.pk_step = code, slice, step
+    raise ex
+
+
+def code_of(ex: BaseException) -> int:
+    """libpk status code of an exception (inverse of raise_for's classes)."""
+    c = getattr(ex, "pk_code", None)
+    if c:
+        return int(c)
+    for code, cls in ((1, SolvabilityViolation), (2, NonFiniteState), (3, StabilityViolation),
+                      (4, MeshTooSmall), (5, ValueError)):
+        if isinstance(ex, cls):
+            return code
+    return 6

@@ -38,7 +38,7 @@ import numpy as np
 from .adaptation import Thresholds
 from . import _native
 from .engine import Device, make_phase
-from .errors import NonFiniteState
+from .errors import NonFiniteState, SimulationError, code_of, raise_for
 from .fluid import FluidStepParams, fluid_propagate, substep_sizes
 from .hybrid import HybridOptions, HybridState, hybrid_propagate, knobs_of
 from .kinetic import KineticStepParams
@@ -237,7 +237,7 @@ class DeviceBackend:
                          [1 if e.sf[n - 1][1] > 0.0 else 0 for n in windows])
         dev.fine(rho, E, Ep, kc, ki, g, self.rb1.expand(B).contiguous(), flags, [ph0, ph1],
                  e.knobs, eps, e.rtol_f)
-        dev.check()
+        dev.check()   # the lowest failing slice (pk_device.cuh set_status)
         return rho, kc.sum(dim=1, dtype=torch.int64)
 
     def jump(self, F, G):
@@ -318,6 +318,18 @@ class _Engine:
         if wins:
             self.G[k + 1:] = self.be.many(self.row[k:self.cfg.ng], wins, self.rtol)
 
+    def correct(self, k, delta):
+        """The sequential correction of iteration k+1 as one chain launch
+        (parareal.py:272-284); a field-guard failure is reported for the
+        window it happened in (the chain stops there)."""
+        try:
+            return self.be.chain(self.row[k], k + 1, self.cfg.ng, delta, self.rtol)
+        except SimulationError as ex:
+            w = getattr(ex, "pk_step", None)
+            if w is None or w < 0:
+                raise
+            raise_for(code_of(ex), f"correction, window {k + 1 + w}", None, None)
+
     def iterate(self, k):
         torch, cfg, be = self.torch, self.cfg, self.be
         ng, nx = cfg.ng, self.nx
@@ -333,19 +345,33 @@ class _Engine:
         t0 = be.clock()
         size, rank = self.comm.size, self.comm.rank
         if size == 1:
-            Fall, kcount = be.fine(self.row[k:ng], targets)
+            Fall, kcount, fail = _fine_or_fail(be, self.row[k:ng], targets)
+            if fail:
+                raise_for(fail[0], f"window {fail[1]}, step {fail[2]}", fail[1], fail[2])
         else:
-            # cyclic deal; one all-gather of [per + 1, nx] rows per rank (the
-            # extra row carries the kinetic-cell counts)
+            # cyclic deal; one all-gather of [per + 2, nx] rows per rank (extra
+            # rows: the kinetic-cell counts, and this rank's failure record)
             per = -(-B // size)
-            assert per <= nx, "window share exceeds the gather row width"
+            assert per <= nx and nx >= 3, "window share exceeds the gather row width"
             mine = targets[rank::size]
-            buf = torch.zeros((per + 1, nx), dtype=torch.float64, device=self.row.device)
+            buf = torch.zeros((per + 2, nx), dtype=torch.float64, device=self.row.device)
             if mine:
-                Fr, kc = be.fine(self.row[[n - 1 for n in mine]], mine)
-                buf[:len(mine)] = Fr
-                buf[per, :len(mine)] = kc.to(torch.float64)
+                # never raise before the collective: the other ranks would
+                # block in it forever.  Post (code, window, step) instead.
+                Fr, kc, fail = _fine_or_fail(be, self.row[[n - 1 for n in mine]], mine)
+                if fail:
+                    buf[per + 1, :3] = torch.tensor(fail, dtype=torch.float64)
+                else:
+                    buf[:len(mine)] = Fr
+                    buf[per, :len(mine)] = kc.to(torch.float64)
             parts = self.comm.all_gather(buf)
+            fails = [tuple(int(v) for v in p[per + 1, :3].tolist()) for p in parts]
+            fails = [f for f in fails if f[0] != 0]
+            if fails:
+                # every rank raises the lowest failing window's error, as the
+                # reference consumes its window futures in order (parareal.py:260-266)
+                code, win, st = min(fails, key=lambda f: f[1])
+                raise_for(code, f"window {win}, step {st}", win, st)
             Fall = torch.empty((B, nx), dtype=torch.float64, device=self.row.device)
             kcount = torch.empty(B, dtype=torch.int64, device=self.row.device)
             for r, part in enumerate(parts):
@@ -357,7 +383,7 @@ class _Engine:
         t2 = be.clock()
         new = self.row.clone()
         Gn = self.G.clone()
-        out, gout = be.chain(self.row[k], k + 1, ng, delta, self.rtol)
+        out, gout = self.correct(k, delta)
         new[k + 1:] = out
         Gn[k + 1:] = gout
         t3 = be.clock()
@@ -368,6 +394,20 @@ class _Engine:
             fracs[n] = float(kc_h[j]) / nx
         self.row, self.G = new, Gn
         return err, delta, fracs, targets, be.seconds(t0, t1), be.seconds(t2, t3)
+
+
+def _fine_or_fail(be, X, windows):
+    """be.fine over `windows`; a failure is returned as (code, window, step)
+    of the lowest failing window instead of raised (the batch reports its
+    lowest failing slice: pk_device.cuh set_status)."""
+    try:
+        F, kc = be.fine(X, windows)
+        return F, kc, None
+    except (SimulationError, ValueError) as ex:
+        sl = getattr(ex, "pk_slice", None)
+        win = windows[sl] if sl is not None and 0 <= sl < len(windows) else windows[0]
+        st = getattr(ex, "pk_step", None)
+        return None, None, (code_of(ex), win, -1 if st is None else int(st))
 
 
 # Overlap the coarse correction with the next iteration's fine windows on a
@@ -544,10 +584,23 @@ class _Overlap:
             self.host_enqueue_s = time.perf_counter() - self._t_iter
             err = float(eng.be.err_d.item())     # waits for the correction stream only
         self.spec = k + 1 if speculate else None
-        cdev.check_stream(cs)
+        # the reference raises the fine windows' errors (lowest window first)
+        # before any correction error (parareal.py:260-284)
         for n in targets:
             self.ss.wait_event(self.ev_jump[q][n])
-            self.devs[n][q].check_stream(self.ss)
+            try:
+                self.devs[n][q].check_stream(self.ss)
+            except (SimulationError, ValueError) as ex:
+                raise_for(code_of(ex), f"window {n}, step {getattr(ex, 'pk_step', None)}", n,
+                          getattr(ex, "pk_step", None))
+        try:
+            cdev.check_stream(cs)
+        except SimulationError:
+            # one window per launch here: locate the failing window with the
+            # phase-by-phase correction (one launch; it raises for that window)
+            self.sync()
+            eng.correct(k, self.D[q, k + 1:])
+            raise
         delta = self.D[q, k + 1:].clone()
         kc = self.K[q].cpu().numpy()
         fracs = np.zeros(ng + 1)

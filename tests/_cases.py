@@ -11,6 +11,14 @@ def digest(a):
     return hashlib.sha256(a.tobytes()).hexdigest()
 
 
+def cdigest(a):
+    """digest() with every NaN replaced by numpy's canonical quiet NaN: x86
+    and the GPU produce different NaN payloads (tests/golden/make_cfg5_golden.py)."""
+    a = np.array(a, dtype=np.float64, copy=True)
+    a[np.isnan(a)] = np.nan
+    return digest(a)
+
+
 def f_paper(vx, M, x_star):
     w = vx**4 * M
     return lambda x: w[None, :] * (1.0 + 0.9 * np.cos(2.0 * np.pi * x / x_star))[:, None]

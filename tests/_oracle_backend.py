@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 import oracle as O
-from paper_2511_13386_b200.errors import NonFiniteState
+from paper_2511_13386_b200.errors import NonFiniteState, raise_for
 
 
 class OracleBackend:
@@ -53,8 +53,13 @@ class OracleBackend:
     def fine(self, X, windows):
         rows, counts = [], []
         for j, n in enumerate(windows):
-            r, frac = O.fine_window(n, X[j].numpy(), self.g0, self.pcfg, self.eng.kin_p.dt,
-                                    self.grid, self.eng.rho_bar)
+            try:
+                r, frac = O.fine_window(n, X[j].numpy(), self.g0, self.pcfg, self.eng.kin_p.dt,
+                                        self.grid, self.eng.rho_bar)
+            except O.OracleSolvability as ex:   # as the device reports it: lowest slice
+                raise_for(1, str(ex), j, None)
+            except O.OracleNonFinite as ex:
+                raise_for(2, str(ex), j, None)
             rows.append(r)
             counts.append(int(round(frac * self.eng.nx)))
         return torch.from_numpy(np.stack(rows)), torch.tensor(counts, dtype=torch.int64)

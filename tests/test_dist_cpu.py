@@ -49,7 +49,12 @@ def _worker(rank, world, port, case, out_dir):
         cfg = pk.PararealConfig(eps=eps, t_final=T, ng=ng, k_max=kmax, tol=tol,
                                 thresholds=pk.Thresholds(d0, e0),
                                 options=pk.HybridOptions(adaptation=adapt))
-        res = pk.run(cfg, rho, g0.reshape(nx, nv, 1, 1), mesh, rb)
+        try:
+            res = pk.run(cfg, rho, g0.reshape(nx, nv, 1, 1), mesh, rb)
+        except pk.SimulationError as ex:
+            np.savez(os.path.join(out_dir, f"r{world}_{rank}.npz"),
+                     raised=np.array(type(ex).__name__), msg=np.array(str(ex)))
+            return
         np.savez(os.path.join(out_dir, f"r{world}_{rank}.npz"), rows=np.stack(res.ledger.rho),
                  err=np.array(res.ledger.err), frac=res.kinetic_fraction,
                  meta=np.array([res.iterations, res.status == "converged"]))
@@ -61,6 +66,8 @@ CASES = [
     ("off_0.5", 32, 16, 0.5, False, 6, 0.3, 12, 1e-10, 1e-5, 1e-5),
     ("on_1e-4", 32, 16, 1e-4, True, 6, 0.3, 12, 1e-10, 1e-5, 1e-5),
 ]
+# the reference raises SolvabilityViolation in this run (tests/golden: p_on_1e-2_raised)
+RAISING = ("on_1e-2", 32, 16, 1e-2, True, 5, 0.2, 8, 1e-10, 1e-3, 1e-3)
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
@@ -77,3 +84,21 @@ def test_parareal_ranks_gloo(tmp_path, gold, case, world):
         assert np.array_equal(got["err"], d[k + "_err"])
         assert np.array_equal(got["frac"], d[k + "_frac"])
         assert list(got["meta"]) == list(d[k + "_meta"])
+
+
+def test_parareal_ranks_failure_consensus(tmp_path, gold):
+    """A fine window that trips the field guard on ONE rank must not leave the
+    other ranks blocked in the all-gather: every rank raises the same error,
+    that of the lowest failing window (the reference consumes its window
+    futures in order, parareal.py:260-266), identical for 1, 2 and 3 ranks."""
+    import torch.multiprocessing as mp
+
+    assert bool(gold("parareal")["p_on_1e-2_raised"])
+    msgs = set()
+    for world in (1, 2, 3):
+        mp.spawn(_worker, args=(world, _free_port(), RAISING, str(tmp_path)), nprocs=world,
+                 join=True)
+        got = [np.load(tmp_path / f"r{world}_{r}.npz") for r in range(world)]
+        assert {str(g["raised"]) for g in got} == {"SolvabilityViolation"}
+        msgs |= {str(g["msg"]) for g in got}
+    assert len(msgs) == 1 and "window" in next(iter(msgs)), msgs

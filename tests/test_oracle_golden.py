@@ -203,3 +203,24 @@ def test_eps_hybrid_cfg3_window2(gold):
         st = O.restate.hstep(st, dt_f, eps, cfg.delta0, cfg.eta0, cfg.opts, g, rb, cfg.rtol)
     with pytest.raises(O.restate.OracleSolvability):
         O.restate.hstep(st, dt_f, eps, cfg.delta0, cfg.eta0, cfg.opts, g, rb, cfg.rtol)
+
+
+@pytest.mark.parametrize("s", [0, 25])
+def test_cfg5_500_steps_vs_reference(gold, s):
+    """BASELINE cfg5 at the bench's length (500 steps): instance 0 and instance
+    25, which the reference's own stable dt lets blow up (step 406)."""
+    from _cases import cdigest
+    from paper_2511_13386_b200 import configs
+
+    d = gold("cfg5_500")
+    c = configs.cfg5([s])[0]
+    grid = O.make_grid(1024, 128)
+    E0 = O.field(c.rho, c.rho_bar, grid)
+    dt = O.stable_dt(grid, c.eps, e_max=float(np.abs(E0).max()))
+    assert dt == d["dt"][s] and c.rho_bar == d["rho_bar"][s]
+    with np.errstate(all="ignore"):
+        r, E, gg = O.kinetic_steps(c.rho, c.g.reshape(1024, 128), 500, dt, c.eps, grid, c.rho_bar)
+    assert cdigest(r) == d["rho_digest"][s]
+    assert cdigest(E) == d["E_digest"][s]
+    assert cdigest(gg) == d["g_digest"][s]
+    assert np.isfinite(r).all() == (d["blowup_step"][s] < 0)
