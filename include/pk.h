@@ -105,6 +105,12 @@ int32_t pk_version(void);
  * prepare, barrier, steps], [6..31] slice-phase sub-timers and counts,
  * [32 + 3c ..] CTA c's [micro, first-barrier wait, SM id]; NULL disables. */
 int32_t pk_debug_profile(pk_ctx* ctx, void* dev_counters);
+/* measurement: accumulate, per slice b of every following pk_fine_propagate
+ * launch, the interface rows the micro phases streamed (kinetic rows, all
+ * steps) at dev_counts[2b] and the rows zeroed (kinetic->fluid) at
+ * dev_counts[2b+1] (device int64 [2B]); NULL disables.  The hybrid roofline's
+ * algorithmic bytes are 16 B x nv x rows + 8 B x nv x zeroed rows. */
+int32_t pk_count_rows(pk_ctx* ctx, void* dev_counts);
 /* diagnostics: how the calling thread's last pk_fine_propagate launch was
  * laid out: out[0] CTAs per thread-block cluster (or software group), out[1]
  * slices per cluster, out[2] 1 when the slice vectors were kept in shared

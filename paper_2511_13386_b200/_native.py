@@ -60,6 +60,7 @@ class PkStatus(C.Structure):
 SIGNATURES = {
     "pk_version": (C.c_int32, []),
     "pk_debug_profile": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "pk_count_rows": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "pk_create": (C.c_void_p, [C.c_int32, C.POINTER(PkMesh)]),
     "pk_destroy": (None, [C.c_void_p]),
     "pk_last_error": (C.c_char_p, [C.c_void_p]),

@@ -40,6 +40,7 @@ struct pk_ctx {
   uint8_t* u8ws = nullptr;  // 7 arrays
   int* iws = nullptr;       // klist cap*nx, nk cap, abort cap
   long long* prof = nullptr;  // optional device phase counters (pk_debug_profile)
+  long long* rowcnt = nullptr;  // optional per-slice row counters (pk_count_rows)
   std::string err;
 };
 
@@ -169,6 +170,7 @@ void bind_ws(pk_ctx* c, pk::FineArgs& a) {
   a.sg_cnt = reinterpret_cast<unsigned*>(a.nzl + c->cap);
   a.status = c->d_status;
   a.prof = c->prof;
+  a.rowcnt = c->rowcnt;
 }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -182,6 +184,12 @@ int32_t pk_version(void) { return 1; }
 int32_t pk_debug_profile(pk_ctx* c, void* dev_counters) {
   if (!c) return PK_ERR_BAD_ARG;
   c->prof = reinterpret_cast<long long*>(dev_counters);
+  return PK_OK;
+}
+
+int32_t pk_count_rows(pk_ctx* c, void* dev_counts) {
+  if (!c) return PK_ERR_BAD_ARG;
+  c->rowcnt = reinterpret_cast<long long*>(dev_counts);
   return PK_OK;
 }
 

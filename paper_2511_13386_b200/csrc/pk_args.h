@@ -84,6 +84,7 @@ struct FineArgs {
   int* abort_;           // [B]
   Status* status;
   long long* prof;       // [6] optional phase profile (pk_debug_profile), or null
+  long long* rowcnt;     // [2B] optional per-slice row counters (pk_count_rows), or null
 };
 
 struct LiftArgs {

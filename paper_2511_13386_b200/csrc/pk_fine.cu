@@ -2304,13 +2304,18 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
   long long tp[6] = {0, 0, 0, 0, 0, 0};
   long long c0 = prof ? clock64() : 0, c1;
   if (prof) a.prof[6] += c0 - t_kstart;  // prologue
+  // optional row counters (pk_count_rows): the slice owner's thread 0
+  const bool rcnt = a.rowcnt && leader && threadIdx.x == 0;
+  long long rc_rows = 0, rc_zero = 0;
   for (int s = 0; s < nst_all; ++s) {
     const int ph = s < n0 ? 0 : 1;
     if constexpr (AD) {  // rows the slice phase listed for zeroing in this step's output
       const int nzr = __ldcg(v.nzl);
       for (int q = wg; q < nzr; q += nwg)
         row_zero_store<T>(buf(s + 1) + (size_t)__ldcg(v.zlist + q) * nv, threadIdx.x & 31, nv);
+      if (rcnt && s < nst) rc_zero += nzr;
     }
+    if (rcnt && s < nst) rc_rows += AD ? __ldcg(v.nk) : nx;
     if (profc) pc_t = clock64();
     if constexpr (G < 0) {
       const int nkk = __ldcg(v.nk);
@@ -2387,6 +2392,10 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
     for (int k = 0; k < 5; ++k) a.prof[k] += tp[k];
     a.prof[5] += nst;
     a.prof[15] = a.local_smem;
+  }
+  if (rcnt) {
+    a.rowcnt[2 * (size_t)b] += rc_rows;
+    a.rowcnt[2 * (size_t)b + 1] += rc_zero;
   }
   // ---- epilogue: leader-local state back to the caller's arrays ----
   if (K > 1 && __ldcg(abort_flag)) return;  // as a single-slice cluster would have

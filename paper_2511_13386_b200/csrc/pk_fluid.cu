@@ -123,6 +123,181 @@ __global__ void __launch_bounds__(NT) chain_kernel(const ChainArgs a) {
     for (int i = threadIdx.x; i < nx; i += NT) a.Eout[(size_t)c * nx + i] = E[i] - mean;
 }
 
+
+// ---------------------------------------------------------------------------
+// Fast mode (exact_scan == 0): the same chain with the field's prefix sum as a
+// parallel scan (SURVEY §7 "hard parts": not bitwise -- the prefix differs
+// from np.cumsum by O(n u |E|) -- so the defect and mean reductions are plain
+// trees too).  The whole state lives in registers: thread t owns the PER
+// consecutive cells [t PER, t PER + PER) of rho and E; the only cross-thread
+// data are the reductions and each thread's edge cells (first rho, last rho,
+// last E) in shared memory.  One step = flux + update in registers, then
+// three block barriers: (1) defect and sum|rho| (guard), (2) the scan and,
+// folded into the same barrier, the sum of E for the zero-mean gauge
+// (sum_t E = sum_w C_w off_w + A_w with per-warp partials), (3) the new edges.
+// cfg4's nx = 8192: 1024 threads x 8 cells.
+struct FastRed {
+  double a[2][32], b[2][32], c[2][32];   // per-warp partials, double-buffered
+};
+
+template <int PER>
+__global__ void __launch_bounds__(PER >= 8 ? 1024 : 512, 1) chain_fast_kernel(const ChainArgs a) {
+  __shared__ FastRed red;
+  __shared__ double firstR[1024], lastR[1024], lastE[1024];
+  const MeshDev& m = a.m;
+  const int nx = m.nx;
+  const int c = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nwarp = blockDim.x >> 5;
+  const int tl = (nx - 1) / PER;               // last thread that owns cells
+  const int i0 = t * PER;
+  const int cnt = t <= tl ? min(PER, nx - i0) : 0;
+  const double dx = m.dx, rdx = m.rdx;
+  const double rb = a.rho_bar[c];
+  double r[PER], e[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    r[k] = k < cnt ? a.rho_in[(size_t)c * nx + i0 + k] : 0.0;
+    e[k] = 0.0;
+  }
+  int par = 0;
+  // publish this thread's edge cells, then one barrier
+  auto edges = [&]() {
+    if (cnt > 0) {
+      firstR[t] = r[0];
+      double lr = r[0], le = e[0];
+#pragma unroll
+      for (int k = 1; k < PER; ++k)
+        if (k < cnt) { lr = r[k]; le = e[k]; }
+      lastR[t] = lr;
+      lastE[t] = le;
+    }
+    __syncthreads();
+  };
+  auto warp_sum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(FULL, v, o);
+    return v;
+  };
+  // field of r into e (poisson.py:41-54 with a parallel prefix); false on a
+  // solvability violation (uniform across the block)
+  auto field = [&]() -> bool {
+    double ls = 0.0, la = 0.0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (k < cnt) {
+        e[k] = (r[k] - rb) * dx;
+        ls = ls + e[k];
+        la = la + fabs(r[k]);
+      }
+    ls = warp_sum(ls);
+    la = warp_sum(la);
+    if (lane == 0) { red.a[par][warp] = ls; red.b[par][warp] = la; }
+    __syncthreads();
+    const double defect = warp_sum(lane < nwarp ? red.a[par][lane] : 0.0);
+    const double abssum = warp_sum(lane < nwarp ? red.b[par][lane] : 0.0);
+    if (fabs(defect) > a.rtol * fmax(abssum * dx, 2.2250738585072014e-308)) return false;
+    const double corr = defect / (double)nx;
+    double acc = 0.0, psum = 0.0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (k < cnt) {
+        acc = acc + (e[k] - corr);
+        e[k] = acc;          // local inclusive prefix
+        psum = psum + acc;
+      }
+    // warp scan of the thread totals
+    double inc = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc = inc + y;
+    }
+    double exc = __shfl_up_sync(FULL, inc, 1);
+    if (lane == 0) exc = 0.0;
+    // sum of this warp's E values up to the warp offset: A_w = sum_t (cnt exc + psum)
+    const double aw = warp_sum((double)cnt * exc + psum);
+    const double cw = warp_sum((double)cnt);
+    if (lane == 31) red.a[par ^ 1][warp] = inc;   // warp total
+    if (lane == 0) { red.b[par ^ 1][warp] = aw; red.c[par ^ 1][warp] = cw; }
+    __syncthreads();
+    par ^= 1;
+    // warp offsets (exclusive scan of the warp totals) and sum(E)
+    double tw = lane < nwarp ? red.a[par][lane] : 0.0;
+    double wi = tw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(FULL, wi, o);
+      if (lane >= o) wi = wi + y;
+    }
+    double we = __shfl_up_sync(FULL, wi, 1);
+    if (lane == 0) we = 0.0;
+    const double tot = warp_sum(lane < nwarp ? red.c[par][lane] * we + red.b[par][lane] : 0.0);
+    const double mean = tot / (double)nx;
+    const double off = __shfl_sync(FULL, we, warp) + exc;
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (k < cnt) e[k] = (off + e[k]) - mean;
+    return true;
+  };
+
+  edges();
+  bool have_E = false;
+  for (int w = 0; w < a.nwin; ++w) {
+    const size_t cw = (size_t)c * a.nwin + w;
+    const int nfull = a.nfull[cw];
+    const double rem = a.rem[cw];
+    if (nfull > 0 || rem > 0.0) {
+      if (w == 0 && a.E_in) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+          if (k < cnt) e[k] = a.E_in[(size_t)c * nx + i0 + k];
+      } else if (!field()) {
+        if (t == 0) set_status(a.status, PK_ERR_SOLVABILITY, c, w);
+        return;
+      }
+      edges();
+      have_E = true;
+      const int nstep = nfull + (rem > 0.0 ? 1 : 0);
+      for (int s = 0; s < nstep; ++s) {
+        const double cflu = s < nfull ? a.cflu_full[cw] : a.cflu_rem[cw];
+        if (cnt > 0) {
+          const int tp = t > 0 ? t - 1 : tl, tn = t < tl ? t + 1 : 0;
+          const double rp = lastR[tp], ep = lastE[tp], rn = firstR[tn];
+          // J_{i-1/2} of the first cell from the neighbour's last cell (fluid.py:51-57)
+          double Jp = qdiv(r[0] - rp, dx, rdx) - ep * 0.5 * (rp + r[0]);
+#pragma unroll
+          for (int k = 0; k < PER; ++k)
+            if (k < cnt) {
+              const double rnk = (k + 1 < cnt) ? r[k + 1] : rn;
+              const double Ji = qdiv(rnk - r[k], dx, rdx) - e[k] * 0.5 * (r[k] + rnk);
+              r[k] = r[k] + cflu * (Ji - Jp);
+              Jp = Ji;
+            }
+        }
+        if (!field()) {
+          if (t == 0) set_status(a.status, PK_ERR_SOLVABILITY, c, w);
+          return;
+        }
+        edges();
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (k < cnt) {
+        const size_t o = cw * nx + i0 + k;
+        if (a.gout) a.gout[o] = r[k];
+        if (a.delta) r[k] = r[k] + a.delta[o];   // parareal.py:281
+        a.out[o] = r[k];
+      }
+    if (a.delta) edges();
+  }
+  if (a.Eout && have_E)
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (k < cnt) a.Eout[(size_t)c * nx + i0 + k] = e[k];
+}
+
 size_t chain_smem_bytes(int nx) {
   return (sizeof(PwPlan) + 15) / 16 * 16 + (size_t)2 * nx * 8 + 2 * (MAX_LEAF + MAX_NODE) * 8;
 }
@@ -140,6 +315,17 @@ cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st) {
     kern<<<a.nchain, nt, smem, st>>>(a);
     return cudaGetLastError();
   };
+  if (!a.exact_scan && nx <= 8192) {
+    // fast mode: registers only, PER cells per thread, <= 1024 threads
+    auto fast = [&](auto kern, int per) {
+      const int nt = ((nx + per - 1) / per + 31) / 32 * 32;
+      kern<<<a.nchain, nt, 0, st>>>(a);
+      return cudaGetLastError();
+    };
+    if (nx <= 1024) return fast(chain_fast_kernel<2>, 2);
+    if (nx <= 2048) return fast(chain_fast_kernel<4>, 4);
+    return fast(chain_fast_kernel<8>, 8);
+  }
   // more threads for the element passes at large nx (the scan stays on one)
   if (nx <= 512) return go(chain_kernel<2, 256>, 256);
   if (nx <= 1024) return go(chain_kernel<4, 256>, 256);

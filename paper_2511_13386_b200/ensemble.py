@@ -62,13 +62,16 @@ class Ensemble:
                           non_blocking=non_blocking)
 
     def prepared(self, nsteps):
-        p = self._prep.get(nsteps)
+        from . import engine
+
+        key = (nsteps, engine.EXACT)
+        p = self._prep.get(key)
         if p is None:
             ph0 = make_phase(self.mesh, self.eps, self.dt, [nsteps] * self.B)
             ph1 = make_phase(self.mesh, self.eps, self.dt, [0] * self.B)
-            p = self._prep[nsteps] = ((ph0, ph1),
-                                      self.dev.prepare_fine(self.B, [ph0, ph1], HybridKnobs(),
-                                                            self.eps))
+            p = self._prep[key] = ((ph0, ph1),
+                                   self.dev.prepare_fine(self.B, [ph0, ph1], HybridKnobs(),
+                                                         self.eps))
         return p
 
     def run(self, nsteps: int, check: bool = True):

@@ -150,9 +150,16 @@ class _Comm:
             pass
 
     def all_gather(self, t):
+        """NCCL gathers device tensors directly (NVLink); a host-side backend
+        (gloo: CPU test runs, or several ranks sharing one GPU) is staged
+        through host memory."""
         if self.size == 1:
             return [t]
         import torch
+        if t.is_cuda and self.dist.get_backend() != "nccl":
+            parts = [torch.empty(t.shape, dtype=t.dtype) for _ in range(self.size)]
+            self.dist.all_gather(parts, t.detach().cpu().contiguous())
+            return [p.to(t.device) for p in parts]
         parts = [torch.empty_like(t) for _ in range(self.size)]
         self.dist.all_gather(parts, t.contiguous())
         return parts
@@ -442,7 +449,9 @@ class _Overlap:
         streams.  At most OVERLAP_CACHE schedules are kept; an evicted one is
         synchronised before its contexts and buffers are released."""
         cfg = eng.cfg
-        key = (id(eng.mesh), str(eng.be.device), cfg.ng, id(cfg.eps), eng.kin_p.dt,
+        from . import engine as _eng
+
+        key = (_eng.EXACT, id(eng.mesh), str(eng.be.device), cfg.ng, id(cfg.eps), eng.kin_p.dt,
                eng.fluid_p.dt, eng.fluid_p.m2, eng.rtol_f, repr(eng.knobs), tuple(eng.sf),
                tuple(eng.sc))
         ov = cls._cache.pop(key, None)
