@@ -21,12 +21,15 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--rtol", type=float, default=1e-5)
+    ap.add_argument("--fast", action="store_true", help="fast scan mode (pk.scan_mode(False))")
     a = ap.parse_args()
     import torch
 
     import paper_2511_13386_b200 as pk
-    from paper_2511_13386_b200 import configs
+    from paper_2511_13386_b200 import configs, engine
     from paper_2511_13386_b200.engine import Device, make_phase
+
+    engine.EXACT = not a.fast
 
     c = configs.cfg4() if a.cfg == 4 else configs.cfg3()
     m = c.mesh
