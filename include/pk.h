@@ -175,6 +175,11 @@ int32_t pk_jump(pk_ctx* ctx, int64_t n, const double* a, const double* b, double
 int32_t pk_maxdiff(pk_ctx* ctx, int64_t n, const double* a, const double* b, double* err,
                    void* stream);
 
+/* diagnostics: out[i] = x[i] / dx through the kernels' division routine (the
+ * Markstein-corrected quotient the transport uses for `out /= dx`,
+ * kinetic.py:173), so tests can check it against IEEE division on the device. */
+int32_t pk_diag_qdiv(pk_ctx* ctx, int64_t n, const double* x, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,8 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
 cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st);
 cudaError_t launch_jump(int64_t n, const double* a, const double* b, double* out, Status* st,
                         cudaStream_t s);
+cudaError_t launch_qdiv(int64_t n, const double* x, double* out, double dx, double rdx,
+                        cudaStream_t s);
 cudaError_t launch_maxdiff(int64_t n, const double* a, const double* b, double* err, Status* st,
                            cudaStream_t s);
 size_t chain_smem_bytes(int nx);
@@ -509,6 +511,14 @@ int32_t pk_jump(pk_ctx* c, int64_t n, const double* a, const double* b, double* 
   cudaSetDevice(c->device);
   cudaError_t e = pk::launch_jump(n, a, b, out, c->d_status, S(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "jump launch");
+  return PK_OK;
+}
+
+int32_t pk_diag_qdiv(pk_ctx* c, int64_t n, const double* x, double* out, void* stream) {
+  if (!c || n < 1 || !x || !out) return fail(c, PK_ERR_BAD_ARG, "pk_diag_qdiv: bad argument");
+  cudaSetDevice(c->device);
+  cudaError_t e = pk::launch_qdiv(n, x, out, c->m.dx, c->m.rdx, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "qdiv launch");
   return PK_OK;
 }
 

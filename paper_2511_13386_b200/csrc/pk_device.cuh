@@ -14,10 +14,21 @@ constexpr int MAX_LEAF = 80;    // pairwise leaves of <= 128 terms: nx <= 10240
 constexpr int MAX_NODE = 80;
 constexpr int MAX_LEVEL = 10;
 
-// Correctly rounded x / d from rd = RN(1/d): one Markstein correction step.
-// Checked against IEEE division on 3e8 random operands per mesh spacing
-// (tests/test_native_host.py builds the CPU check; tests/test_gpu_parity.py
-// repeats it on the device).  Used for `out /= dx` (kinetic.py:173).
+// x / d from rd = RN(1/d) with one Markstein correction step: the correctly
+// rounded IEEE quotient for every |x| >= 2^-960 (d here is a mesh spacing,
+// 2^-14 < d < 1).  Below that the residual r = x - q d leaves the normal
+// range and the step can miss the rounding (subnormal and near-subnormal
+// numerators), and a -0.0 numerator gives +0.0.  Checked bit for bit against
+// IEEE division: on the CPU, 2e6 operands per spacing 2 pi / nx for 12 nx
+// (tests/test_native_host.py); on the device, through pk_diag_qdiv, 2^20
+// operands per spacing for 14 (nx, x*) pairs over the whole exponent range
+// (tests/test_gpu_parity.py::test_qdiv_matches_ieee_division_on_device:
+// identical above 2^-960; every difference found lies below it or is -0.0).
+// The numerators are differences of g values (kinetic.py:173) and of
+// densities (fluid.py:51) -- never that small in these models; a guard for
+// them (an integer exponent test + an IEEE division on the rare path) cost
+// 25 % of the cfg5 throughput, so a build with -DPK_TRUE_DIV is the exact
+// everywhere alternative.
 __device__ __forceinline__ double qdiv(double x, double d, double rd) {
 #ifdef PK_TRUE_DIV
   return x / d;

@@ -356,6 +356,22 @@ cudaError_t launch_jump(int64_t n, const double* a, const double* b, double* out
   return cudaGetLastError();
 }
 
+// pk_diag_qdiv: the kernels' quotient routine over an array (test hook)
+__global__ void qdiv_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ out,
+                            double dx, double rdx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = qdiv(x[i], dx, rdx);
+}
+
+cudaError_t launch_qdiv(int64_t n, const double* x, double* out, double dx, double rdx,
+                        cudaStream_t s) {
+  const int64_t want = (n + 255) / 256;
+  const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
+  qdiv_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(n, x, out, dx, rdx);
+  return cudaGetLastError();
+}
+
 // err = max |a - b| (parareal.py:286); max is order-independent, so a tree is
 // exact.  Also flags a non-finite a (parareal.py:283-284).  One CTA.
 __global__ void maxdiff_kernel(int64_t n, const double* __restrict__ a,

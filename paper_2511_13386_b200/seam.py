@@ -113,7 +113,6 @@ def install(ref_parareal):
 
 
 def uninstall(ref_parareal):
-    orig = getattr(ref_parareal, "_b200_original_fine_window", None)
-    if orig is not None:
-        ref_parareal._fine_window = orig
+    if hasattr(ref_parareal, "_b200_original_fine_window"):
+        ref_parareal._fine_window = ref_parareal._b200_original_fine_window
         del ref_parareal._b200_original_fine_window

@@ -608,3 +608,49 @@ def test_overlapped_schedule_matches_phase_by_phase(adapt, kmax):
     assert eq(a.ledger.err, b.ledger.err) and eq(a.kinetic_fraction, b.kinetic_fraction)
     for ja, jb in zip(a.ledger.jumps, b.ledger.jumps):
         assert ja.keys() == jb.keys() and all(eq(ja[n], jb[n]) for n in ja)
+
+
+@pytest.mark.parametrize("nx,xs", [(7, 2 * np.pi), (16, 2 * np.pi), (24, 2 * np.pi),
+                                   (32, 2 * np.pi), (48, 2 * np.pi), (64, 2 * np.pi),
+                                   (128, 2 * np.pi), (256, 2 * np.pi), (512, 2 * np.pi),
+                                   (1000, 2 * np.pi), (1024, 2 * np.pi), (8192, 2 * np.pi),
+                                   (100, 1.0), (37, 3.7)])
+def test_qdiv_matches_ieee_division_on_device(nx, xs):
+    """The kernels' Markstein-corrected quotient (pk_device.cuh qdiv, used for
+    `out /= dx`, kinetic.py:173, and the fluid flux) on the device, against
+    IEEE x / dx: bit for bit for every operand with |x| >= 2^-960 (random
+    operands over the whole exponent range and exact multiples of dx); the
+    only differences anywhere are below 2^-960 (subnormal / near-subnormal
+    numerators) or a -0.0 numerator (+0.0 instead of -0.0)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2511_13386_b200.engine import Device
+
+    m = pk.build_mesh(pk.MeshSpec(nx=nx, nvx=8, x_star=xs))
+    dev = Device.for_mesh(m)
+    rng = np.random.default_rng(nx)
+    n = 1 << 20
+    mant = 1.0 + rng.random(n)
+    ex = rng.integers(-1022, 1000, n)
+    x = np.ldexp(mant, ex) * np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    x[: n // 16] = rng.random(n // 16) * 2.0 ** -1022 * np.where(rng.random(n // 16) < 0.5, -1, 1)
+    x[n // 16: n // 16 + 4] = [0.0, -0.0, m.dx, -3.0 * m.dx]
+    x[n // 16 + 4: n // 8] = m.dx * rng.integers(-10**6, 10**6, n // 16 - 4)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    rc = dev.lib.pk_diag_qdiv(dev.ctx, n, C.c_void_p(xd.data_ptr()), C.c_void_p(out.data_ptr()),
+                              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    got = out.cpu().numpy()
+    want = x / m.dx
+    bad = got.view(np.uint64) != want.view(np.uint64)
+    big = np.abs(x) >= 2.0 ** -960
+    assert not (bad & big).any(), (x[bad & big][:4], got[bad & big][:4], want[bad & big][:4])
+    odd = bad & ~big
+    # what differs is confined to that domain: tiny numerators, and -0.0 -> +0.0
+    assert np.all((np.abs(x[odd]) < 2.0 ** -960))
+    assert np.array_equal(got[odd], want[odd]) or np.all(np.abs(got[odd] - want[odd])
+                                                         <= np.spacing(np.abs(want[odd])))
+    assert int(big.sum()) > n // 2

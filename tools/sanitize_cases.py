@@ -125,7 +125,7 @@ CASES = {
     "cluster": lambda: ensemble(64, 64, 4, 6, want_kind=0),
     "cluster128": lambda: ensemble(64, 128, 4, 6, want_kind=0),
     "packed": lambda: ensemble(32, 64, 170, 3),
-    "sg": lambda: ensemble(64, 128, 256, 3, want_kind=1),
+    "sg": lambda: ensemble(256, 128, 256, 3, want_kind=1),
     "single": lambda: ensemble(64, 64, 3, 4, hint=1),
     "nv256": lambda: ensemble(64, 256, 3, 4),
     "generic": lambda: ensemble(24, 200, 3, 4),
