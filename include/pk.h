@@ -167,6 +167,21 @@ int32_t pk_lift(pk_ctx* ctx, int32_t B, const double* rho, const double* E,
                 int32_t order, int32_t time_elim, int32_t project,
                 double* g_out, void* stream);
 
+/* --- adaptation indicators (adaptation.py:120-181) ----------------------
+ * The public K3 operators as standalone calls, in the arithmetic F uses every
+ * step (pk_fine_propagate computes them in-kernel).  Replace:
+ *   remainder_indicator / remainder_from_fields (adaptation.py:120-152):
+ *     R[B*nx] from rho, E and either E_prev with dt (dE/dt = (E-E_prev)/dt
+ *     averaged to cells) or the cell-centred dE/dt dtE_c (E_prev = NULL);
+ *   perturbation_indicator (adaptation.py:155-159): gnorm[B*nx] from g;
+ *   update_labels (adaptation.py:162-181): kc/ki[B*nx] (uint8 0/1). */
+int32_t pk_remainder(pk_ctx* ctx, int32_t B, const double* rho, const double* E,
+                     const double* E_prev, const double* dtE_c, double dt, const double* rho_bar,
+                     double* R, void* stream);
+int32_t pk_perturbation(pk_ctx* ctx, int32_t B, const double* g, double* gnorm, void* stream);
+int32_t pk_labels(pk_ctx* ctx, int32_t B, const double* R, const double* gnorm, double delta0,
+                  double eta0, int32_t combine_and, uint8_t* kc, uint8_t* ki, void* stream);
+
 /* --- parareal glue (parareal.py:267-289) -------------------------------- */
 /* out[i] = a[i] - b[i] over n values; flags non-finite into the status. */
 int32_t pk_jump(pk_ctx* ctx, int64_t n, const double* a, const double* b, double* out,

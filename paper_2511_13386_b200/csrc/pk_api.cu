@@ -15,6 +15,7 @@ namespace pk {
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st);
 void fine_last_launch(int out[4]);
 cudaError_t launch_lift(const LiftArgs& a, cudaStream_t st);
+cudaError_t launch_indicators(const IndArgs& a, int which, cudaStream_t st);
 cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
 cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st);
 cudaError_t launch_jump(int64_t n, const double* a, const double* b, double* out, Status* st,
@@ -511,6 +512,61 @@ int32_t pk_jump(pk_ctx* c, int64_t n, const double* a, const double* b, double* 
   cudaSetDevice(c->device);
   cudaError_t e = pk::launch_jump(n, a, b, out, c->d_status, S(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "jump launch");
+  return PK_OK;
+}
+
+int32_t pk_remainder(pk_ctx* c, int32_t B, const double* rho, const double* E,
+                     const double* E_prev, const double* dtE_c, double dt, const double* rho_bar,
+                     double* R, void* stream) {
+  if (!c || B < 1 || !rho || !E || !rho_bar || !R || (!E_prev && !dtE_c))
+    return fail(c, PK_ERR_BAD_ARG, "pk_remainder: bad argument");
+  if (c->m.nx < 7) return fail(c, PK_ERR_MESH_TOO_SMALL, "stencils need at least 7 points");
+  cudaSetDevice(c->device);
+  pk::IndArgs a{};
+  a.m = c->m;
+  a.B = B;
+  a.rho = rho;
+  a.E = E;
+  a.E_prev = E_prev;
+  a.dtE_c = dtE_c;
+  a.dt = dt;
+  a.rho_bar = rho_bar;
+  a.R = R;
+  cudaError_t e = pk::launch_indicators(a, 0, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "remainder launch");
+  return PK_OK;
+}
+
+int32_t pk_perturbation(pk_ctx* c, int32_t B, const double* g, double* gnorm, void* stream) {
+  if (!c || B < 1 || !g || !gnorm) return fail(c, PK_ERR_BAD_ARG, "pk_perturbation: bad argument");
+  cudaSetDevice(c->device);
+  pk::IndArgs a{};
+  a.m = c->m;
+  a.B = B;
+  a.g = g;
+  a.gnorm = gnorm;
+  cudaError_t e = pk::launch_indicators(a, 1, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "perturbation launch");
+  return PK_OK;
+}
+
+int32_t pk_labels(pk_ctx* c, int32_t B, const double* R, const double* gnorm, double delta0,
+                  double eta0, int32_t combine_and, uint8_t* kc, uint8_t* ki, void* stream) {
+  if (!c || B < 1 || !R || !gnorm || !kc || !ki)
+    return fail(c, PK_ERR_BAD_ARG, "pk_labels: bad argument");
+  cudaSetDevice(c->device);
+  pk::IndArgs a{};
+  a.m = c->m;
+  a.B = B;
+  a.Rin = R;
+  a.gin = gnorm;
+  a.delta0 = delta0;
+  a.eta0 = eta0;
+  a.combine_and = combine_and;
+  a.kc = kc;
+  a.ki = ki;
+  cudaError_t e = pk::launch_indicators(a, 2, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "labels launch");
   return PK_OK;
 }
 

@@ -100,6 +100,26 @@ struct LiftArgs {
   double *J, *tA, *tB, *tC, *tD, *tE;  // workspace [B*nx]
 };
 
+// Standalone adaptation indicators (adaptation.py:120-181), one CTA per slice.
+struct IndArgs {
+  MeshDev m;
+  int B;
+  const double* rho;      // [B*nx]           remainder
+  const double* E;        // [B*nx]
+  const double* E_prev;   // [B*nx] or null   (E - E_prev) / dt ...
+  const double* dtE_c;    // [B*nx] or null   ... or this cell-centred dE/dt
+  double dt;
+  const double* rho_bar;  // [B]
+  double* R;              // [B*nx] out
+  const double* g;        // [B*nx*nv]        perturbation norm
+  double* gnorm;          // [B*nx] out
+  const double* Rin;      // [B*nx]           labels from (R, gnorm)
+  const double* gin;      // [B*nx]
+  double delta0, eta0;
+  int combine_and;
+  uint8_t *kc, *ki;       // [B*nx] out
+};
+
 struct FieldArgs {
   MeshDev m;
   int B, exact_scan;

@@ -2745,6 +2745,106 @@ cudaError_t launch_lift(const LiftArgs& a, cudaStream_t st) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Standalone adaptation indicators (adaptation.py:120-181): the public K3
+// operators on the device, in the arithmetic of prepare_step (the in-kernel
+// copy F uses every step).  One CTA per slice.
+
+// R = -D3(J_c) + E_c D2(J_c) + (2 rho - 3 rho_bar) D1(J_c) + 2 J_c D1(rho)
+//     - D1(rho) dtE_c   (remainder_from_fields / remainder_indicator,
+// adaptation.py:120-152)
+__global__ void __launch_bounds__(256) remainder_kernel(const IndArgs a) {
+  extern __shared__ __align__(16) double ism[];
+  const MeshDev& m = a.m;
+  const int nx = m.nx, b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const size_t o = (size_t)b * nx;
+  const double* rho = a.rho + o;
+  const double* E = a.E + o;
+  double* J = ism;         // fluid_flux at interfaces, then dE/dt at interfaces
+  double* Jc = ism + nx;   // J_c at cells
+  double* dE = ism;
+  for (int i = tid; i < nx; i += nt) J[i] = flux_J(rho[i], rho[wrap(i + 1, nx)], E[i], m.dx, m.rdx);
+  __syncthreads();
+  for (int i = tid; i < nx; i += nt) Jc[i] = 0.5 * (J[wrap(i - 1, nx)] + J[i]);
+  __syncthreads();
+  for (int i = tid; i < nx; i += nt)
+    dE[i] = a.dtE_c ? a.dtE_c[o + i] : (E[i] - a.E_prev[o + i]) / a.dt;
+  __syncthreads();
+  const double three_rb = 3.0 * a.rho_bar[b];
+  for (int i = tid; i < nx; i += nt) {
+    const int ip = wrap(i - 1, nx);
+    const double dtEc = a.dtE_c ? dE[i] : 0.5 * (dE[ip] + dE[i]);
+    const double Ec = 0.5 * (E[ip] + E[i]);
+    const double d1J = stencil_at(Jc, i, nx, m, 1);
+    const double d2J = stencil_at(Jc, i, nx, m, 2);
+    const double d3J = stencil_at(Jc, i, nx, m, 3);
+    const double d1r = stencil_at(rho, i, nx, m, 1);
+    a.R[o + i] = -d3J + Ec * d2J + (2.0 * rho[i] - three_rb) * d1J + 2.0 * Jc[i] * d1r -
+                 d1r * dtEc;
+  }
+}
+
+// gnorm_i = sqrt(0.5 (<g^2>_{i-1} + <g^2>_i)) (perturbation_indicator,
+// adaptation.py:155-159); <.> the folded pairwise bracket, one warp per row.
+__global__ void __launch_bounds__(256) gnorm_kernel(const IndArgs a) {
+  extern __shared__ __align__(16) double ism[];
+  const MeshDev& m = a.m;
+  const int nx = m.nx, nv = m.nv, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  double* sq = ism;
+  double* scr = ism + nx + warp * BIG_SCR;
+  const double* g = a.g + (size_t)b * nx * nv;
+  for (int i = warp; i < nx; i += nwarp) {
+    const double* row = g + (size_t)i * nv;
+    const double v = big_bracket([&](int c) { const double x = row[c]; return x * x; }, m, scr);
+    if (lane == 0) sq[i] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nx; i += blockDim.x)
+    a.gnorm[(size_t)b * nx + i] = sqrt(0.5 * (sq[wrap(i - 1, nx)] + sq[i]));
+}
+
+// labels (update_labels, DomainLabels.from_cells; adaptation.py:100-105,162-181)
+__global__ void labels_kernel(const IndArgs a) {
+  const int nx = a.m.nx;
+  const int64_t n = (int64_t)a.B * nx;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = k - k % nx;
+    auto kin = [&](int64_t q) {
+      const bool fR = fabs(a.Rin[q]) < a.delta0;
+      const bool fg = a.gin[q] < a.eta0;
+      return !(a.combine_and ? (fR && fg) : (fR || fg));
+    };
+    const bool kc = kin(k);
+    const int64_t kn = (k + 1 - b0 == nx) ? b0 : k + 1;
+    a.kc[k] = kc ? 1 : 0;
+    a.ki[k] = (kc || kin(kn)) ? 1 : 0;
+  }
+}
+
+cudaError_t launch_indicators(const IndArgs& a, int which, cudaStream_t st) {
+  const int nx = a.m.nx;
+  if (which == 0) {
+    const size_t smem = 2 * (size_t)nx * 8;
+    cudaError_t e = cudaFuncSetAttribute(remainder_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    remainder_kernel<<<a.B, 256, smem, st>>>(a);
+  } else if (which == 1) {
+    const size_t smem = ((size_t)nx + 8 * (size_t)BIG_SCR) * 8;
+    cudaError_t e =
+        cudaFuncSetAttribute(gnorm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    gnorm_kernel<<<a.B, 256, smem, st>>>(a);
+  } else {
+    const int64_t n = (int64_t)a.B * nx;
+    const int64_t want = (n + 255) / 256;
+    labels_kernel<<<(int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8), 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
   // slice_field's block_pairwise2 keeps two reductions in flight
   const size_t smem = (sizeof(PwPlan) + 15) / 16 * 16 + 2 * (MAX_LEAF + MAX_NODE) * 8;

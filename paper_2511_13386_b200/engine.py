@@ -230,13 +230,21 @@ class Device:
         return torch.from_numpy(a).to(self.device, non_blocking=False)
 
     def scratch(self, name, shape, dtype=None):
+        """Named grow-only work buffer: a view of the first prod(shape)
+        elements.  One buffer per (name, dtype) -- a shrinking batch (B = Ng - k
+        active windows) reuses it instead of allocating per distinct shape.
+        Growth synchronises the device first, so no queued kernel (on any
+        stream) still uses the buffer that is dropped."""
         torch = _torch()
         dtype = dtype or torch.float64
-        key = (name, tuple(shape), dtype)
+        n = int(np.prod(shape))
+        key = (name, dtype)
         buf = self._scratch.get(key)
-        if buf is None:
-            buf = self._scratch[key] = torch.empty(shape, dtype=dtype, device=self.device)
-        return buf
+        if buf is None or buf.numel() < n:
+            if buf is not None:
+                torch.cuda.synchronize(self.device)
+            buf = self._scratch[key] = torch.empty(max(n, 1), dtype=dtype, device=self.device)
+        return buf[:n].view(tuple(shape))
 
     def _rc(self, code, what):
         if code != 0:

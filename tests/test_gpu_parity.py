@@ -345,7 +345,15 @@ def test_packed_clusters_match_one_slice_per_cluster(nv, B, sg):
         Cc, K, on_chip, soft = dev.last_launch()
         assert on_chip
         if hint == 0:
-            if not os.environ.get("PK_NO_SG"):  # (the A/B switch turns software groups off)
+            if "PK_NO_SG" in os.environ:  # (the A/B switch turns software groups off)
+                assert soft == 0, (Cc, K, soft)
+                if sg:
+                    # hardware clusters cannot pack this shape: the packed
+                    # fallback would be compared with itself -- say so
+                    pytest.skip("PK_NO_SG: no software groups and no hardware packing "
+                                f"for B={B}, nv={nv} (layout {(Cc, K, soft)})")
+                assert 1 < K < Cc, (Cc, K, soft)
+            else:
                 assert 1 < K < Cc and (sg is None or (soft == 1) == sg), (Cc, K, soft)
         else:
             assert (Cc, K, soft) == (1, 1, 0)
@@ -401,8 +409,10 @@ def test_software_groups_nonfinite_and_mid_run_trips():
         Cc, K, _, soft = dev.last_launch()
         if hint == 1:
             assert (Cc, K, soft) == (1, 1, 0)
-        elif not os.environ.get("PK_NO_SG"):
+        elif "PK_NO_SG" not in os.environ:
             assert soft == 1
+        else:
+            assert soft == 0
         outs.append([tripped] + [x.cpu().numpy() for x in (rho, E, g)])
     assert outs[0][0] == outs[1][0]
     for x0, x1 in zip(outs[0][1:], outs[1][1:]):
@@ -654,3 +664,45 @@ def test_qdiv_matches_ieee_division_on_device(nx, xs):
     assert np.array_equal(got[odd], want[odd]) or np.all(np.abs(got[odd] - want[odd])
                                                          <= np.spacing(np.abs(want[odd])))
     assert int(big.sum()) > n // 2
+
+
+@pytest.mark.parametrize("nx,nv,nvy", [(7, 8, 1), (48, 9, 1), (48, 16, 1), (1000, 64, 1),
+                                       (256, 128, 1), (64, 200, 1), (96, 256, 1), (40, 512, 1),
+                                       (8192, 8, 1), (16, 8, 4), (12, 7, 5), (8, 32, 16)])
+def test_indicator_operators_on_device(nx, nv, nvy):
+    """The public K3 operators (remainder_indicator, remainder_from_fields,
+    perturbation_indicator, update_labels; adaptation.py:120-181) run on the
+    device (pk_remainder / pk_perturbation / pk_labels): bitwise equal to the
+    oracle (1D-1V; pinned to the reference) and, on 1D-3V grids, to the
+    host bracket (bit-identical to the reference's, tests/test_v3.py)."""
+    from paper_2511_13386_b200 import adaptation as A
+
+    m = pk.build_mesh(pk.MeshSpec(nx=nx, nvx=nv, nvy=nvy, nvz=nvy))
+    rng = np.random.default_rng(nx * 1000 + nv)
+    x = m.x_centers
+    rho = 1.0 + 0.3 * np.cos(x) + 0.05 * np.sin(3 * x) + 1e-3 * rng.standard_normal(nx)
+    rb = float(rho.sum() * m.dx / m.x_star)
+    E = pk.solve_field(rho, rb, m, rtol=1.0)
+    Ep = E * (1.0 + 1e-3 * rng.standard_normal(nx))
+    dt = 3.7e-5
+    g = 1e-3 * rng.standard_normal((nx,) + m.vgrid.shape)
+    R = A.remainder_indicator(rho, E, Ep, dt, rb, m)
+    gn = A.perturbation_indicator(g, m)
+    dtc = 0.5 * (np.roll((E - Ep) / dt, 1) + (E - Ep) / dt)
+    R2 = A.remainder_from_fields(rho, E, dtc, rb, m)
+    if nvy == 1:
+        grid = O.make_grid(nx, nv)
+        assert eq(R, O.remainder(rho, E, Ep, dt, rb, grid))
+        assert eq(gn, O.gnorm(g.reshape(nx, nv), grid))
+    else:
+        sq = m.bracket_x(g * g)
+        assert eq(gn, np.sqrt(0.5 * (np.roll(sq, 1) + sq)))
+    assert eq(R2, R)
+    for comb in ("or", "and"):
+        d0 = float(np.median(np.abs(R)))
+        e0 = float(np.median(gn))
+        lab = A.update_labels(R, gn, pk.Thresholds(d0, e0), comb)
+        kc, ki = O.labels_from(R, gn, d0, e0, comb)
+        assert eq(lab.kinetic_cells, kc) and eq(lab.kinetic_ifaces, ki)
+    with pytest.raises(ValueError):
+        A.update_labels(R, gn, pk.Thresholds(1.0, 1.0), "xor")
