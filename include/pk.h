@@ -99,6 +99,11 @@ int32_t pk_status_read(pk_ctx* ctx, pk_status* out, int32_t clear); /* synchroni
 /* Same record, ordered on `stream` only (waits for the work queued on that
    stream, not for the whole device): for contexts driven from several streams. */
 int32_t pk_status_read_stream(pk_ctx* ctx, pk_status* out, int32_t clear, void* stream);
+/* The same record as two doubles in DEVICE memory, dst[0] = code (0: ok),
+   dst[1] = step, stream-ordered without a host synchronisation (the
+   multi-rank engine ships a window's status inside its jump's collective);
+   clear != 0 re-arms the record. */
+int32_t pk_status_store(pk_ctx* ctx, double* dst, int32_t clear, void* stream);
 int32_t pk_version(void);
 /* diagnostics: accumulate clock64 counters into a device array of
  * 32 + 3 * 1024 int64: [0..5] slice 0's [micro, barrier, slice finish, slice

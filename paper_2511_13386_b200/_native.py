@@ -87,6 +87,7 @@ SIGNATURES = {
                             C.c_void_p]),
     "pk_maxdiff": (C.c_int32, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p]),
+    "pk_status_store": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "pk_remainder": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pk_perturbation": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,

@@ -20,6 +20,7 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
 cudaError_t launch_chain(const ChainArgs& a, cudaStream_t st);
 cudaError_t launch_jump(int64_t n, const double* a, const double* b, double* out, Status* st,
                         cudaStream_t s);
+cudaError_t launch_status_store(Status* st, double* dst, int clear, cudaStream_t s);
 cudaError_t launch_qdiv(int64_t n, const double* x, double* out, double dx, double rdx,
                         cudaStream_t s);
 cudaError_t launch_maxdiff(int64_t n, const double* a, const double* b, double* err, Status* st,
@@ -512,6 +513,14 @@ int32_t pk_jump(pk_ctx* c, int64_t n, const double* a, const double* b, double* 
   cudaSetDevice(c->device);
   cudaError_t e = pk::launch_jump(n, a, b, out, c->d_status, S(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "jump launch");
+  return PK_OK;
+}
+
+int32_t pk_status_store(pk_ctx* c, double* dst, int32_t clear, void* stream) {
+  if (!c || !dst) return fail(c, PK_ERR_BAD_ARG, "pk_status_store: bad argument");
+  cudaSetDevice(c->device);
+  cudaError_t e = pk::launch_status_store(c->d_status, dst, clear, S(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "status store launch");
   return PK_OK;
 }
 

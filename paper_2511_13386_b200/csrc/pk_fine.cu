@@ -222,6 +222,108 @@ __device__ __forceinline__ double stencil_reg(const double (&w)[7], const MeshDe
 // E_out = solve_field(rho); false on a solvability violation.
 // poisson.py:41-54: src=(rho-rb)dx; defect=sum(src); guard; src-=defect/nx;
 // E=cumsum(src); E-=mean(E).
+// Fast mode (exact_scan == 0) field of rho into E_out: plain-tree sums and a
+// parallel prefix, two block barriers (poisson.py:41-54 up to reassociation:
+// not bitwise, O(nx u |E|) from np.cumsum).  Warp w owns a contiguous chunk of
+// cells, read in coalesced rounds of 32; within a round a warp scan, the
+// running carry across rounds; the warp offsets and -- folded into the same
+// barrier -- sum(E) for the zero-mean gauge come from per-warp partials
+// (sum_w C_w off_w + A_w).  Works on shared or global vectors alike.
+__device__ bool slice_field_fast(const MeshDev& m, const double* __restrict__ rho, double rb,
+                                 double* __restrict__ E_out, double rtol, double* red) {
+  const int nx = m.nx;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int cw = ((nx + nw - 1) / nw + 31) & ~31;
+  const int lo = min(nx, warp * cw), hi = min(nx, lo + cw);
+  const double dx = m.dx;
+  auto wsum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(FULL, v, o);
+    return v;
+  };
+  constexpr int U = 4;
+  double ls = 0.0, la = 0.0;
+  for (int b = lo; b < hi; b += 32 * U) {
+    double r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      r[u] = i < hi ? rho[i] : rb;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      ls = ls + (r[u] - rb) * dx;
+      la = la + (i < hi ? fabs(r[u]) : 0.0);
+    }
+  }
+  ls = wsum(ls);
+  la = wsum(la);
+  if (lane == 0) {
+    red[warp] = ls;
+    red[32 + warp] = la;
+  }
+  __syncthreads();
+  const double defect = wsum(lane < nw ? red[lane] : 0.0);
+  const double abssum = wsum(lane < nw ? red[32 + lane] : 0.0);
+  if (fabs(defect) > rtol * fmax(abssum * dx, 2.2250738585072014e-308)) return false;
+  const double corr = defect / (double)nx;
+  double carry = 0.0, part = 0.0;
+  for (int b = lo; b < hi; b += 32 * U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      v[u] = i < hi ? (rho[i] - rb) * dx - corr : 0.0;
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double y = __shfl_up_sync(FULL, v[u], o);
+        if (lane >= o) v[u] = v[u] + y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      const double e = carry + v[u];
+      if (i < hi) {
+        E_out[i] = e;
+        part = part + e;
+      }
+      carry = carry + __shfl_sync(FULL, v[u], 31);
+    }
+  }
+  const double aw = wsum(part);
+  if (lane == 0) {
+    red[64 + warp] = carry;                    // warp total
+    red[96 + warp] = aw;                       // sum of the warp-local prefixes
+    red[128 + warp] = (double)(hi - lo);       // cells in the warp
+  }
+  __syncthreads();
+  double wi = lane < nw ? red[64 + lane] : 0.0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(FULL, wi, o);
+    if (lane >= o) wi = wi + y;
+  }
+  double we = __shfl_up_sync(FULL, wi, 1);
+  if (lane == 0) we = 0.0;
+  const double tot = wsum(lane < nw ? red[128 + lane] * we + red[96 + lane] : 0.0);
+  const double mean = tot / (double)nx;
+  const double off = __shfl_sync(FULL, we, warp);
+  for (int b = lo; b < hi; b += 32 * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      if (i < hi) E_out[i] = (off + E_out[i]) - mean;
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
 __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, double* src,
                             double* E_out, double rtol, int exact_scan, bool on_chip,
                             const Smem& sm, long long* dbg = nullptr) {
@@ -232,6 +334,12 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
     const long long c1 = clock64();        \
     dbg[k] += c1 - c0;                     \
     c0 = c1;                               \
+  }
+  if (!exact_scan) {
+    PK_TICK(0)
+    const bool ok = slice_field_fast(m, rho, rb, E_out, rtol, sm.red);
+    PK_TICK(3)
+    return ok;
   }
   if (sm.scan && exact_scan && !on_chip) {
     // global-memory slice vectors with a buffer of scan_cap doubles on chip:

@@ -356,6 +356,26 @@ cudaError_t launch_jump(int64_t n, const double* a, const double* b, double* out
   return cudaGetLastError();
 }
 
+// pk_status_store: the status record as doubles into device memory (code,
+// step), optionally re-armed -- stream-ordered, no host synchronisation, so a
+// window's status can travel in the same collective as its jump.
+__global__ void status_store_kernel(Status* st, double* dst, int clear) {
+  const unsigned long long k = st->key;
+  if (k == ~0ull) {
+    dst[0] = 0.0;
+    dst[1] = 0.0;
+  } else {
+    dst[0] = (double)(int)(k & 0xFF);
+    dst[1] = (double)(int)(unsigned)((k >> 8) & 0xFFFFFFFFull);
+  }
+  if (clear) st->key = ~0ull;
+}
+
+cudaError_t launch_status_store(Status* st, double* dst, int clear, cudaStream_t s) {
+  status_store_kernel<<<1, 1, 0, s>>>(st, dst, clear);
+  return cudaGetLastError();
+}
+
 // pk_diag_qdiv: the kernels' quotient routine over an array (test hook)
 __global__ void qdiv_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ out,
                             double dx, double rdx) {

@@ -55,7 +55,13 @@ def _torch():
 
 
 def _ptr(t):
-    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+    """Device pointer of a tensor for libpk, which reads every array as dense
+    C order: a strided view is refused loudly rather than misread."""
+    if t is None:
+        return C.c_void_p(0)
+    if not t.is_contiguous():
+        raise NativeError(f"libpk needs contiguous arrays (got strides {t.stride()})")
+    return C.c_void_p(t.data_ptr())
 
 
 def relaxation_coefficients(dt: float, eps: float):

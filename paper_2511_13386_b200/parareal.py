@@ -149,6 +149,19 @@ class _Comm:
         except Exception:
             pass
 
+    def broadcast(self, t, src):
+        """Broadcast t from rank src, stream-ordered on the current stream:
+        NCCL returns a work whose wait() makes the current stream wait; a
+        host-side backend (gloo) is staged through host memory (blocking)."""
+        if self.size == 1:
+            return None
+        if t.is_cuda and self.dist.get_backend() != "nccl":
+            h = t.detach().cpu()
+            self.dist.broadcast(h, src)
+            t.copy_(h)
+            return None
+        return self.dist.broadcast(t, src, async_op=True)
+
     def all_gather(self, t):
         """NCCL gathers device tensors directly (NVLink); a host-side backend
         (gloo: CPU test runs, or several ranks sharing one GPU) is staged
@@ -202,7 +215,7 @@ class DeviceBackend:
         gout = self.torch.empty_like(out)
         sc = e.sc[n0 - 1:n1]
         self.dev.chain(x.reshape(1, e.nx), out.reshape(1, W, e.nx), gout.reshape(1, W, e.nx), None,
-                       None if delta is None else delta.reshape(1, W, e.nx),
+                       None if delta is None else delta.contiguous().reshape(1, W, e.nx),
                        [q[0] for q in sc], [q[1] for q in sc], e.fluid_p.dt, self.rb1,
                        SOLVABILITY_RTOL if rtol is None else rtol, m2=e.fluid_p.m2)
         self.dev.check()
@@ -345,7 +358,7 @@ class _Engine:
         if B == 0:
             # every window converged by prefix exactness: row_{k+1} == row_k
             return 0.0, self.row[:0], np.zeros(ng + 1), targets, 0.0, 0.0
-        if self.comm.size == 1 and isinstance(be, DeviceBackend) and OVERLAP:
+        if use_overlap(self):
             if self.overlap is None:
                 self.overlap = _Overlap.get(self)
             return self.overlap.iterate(k)
@@ -424,9 +437,22 @@ TIMELINE = False    # diagnostics: record per-window event times (tools/par_timi
 OVERLAP_CACHE = 2   # schedules (with their contexts and buffers) kept for reuse
 
 
+def use_overlap(eng) -> bool:
+    """The overlapped schedule (below) when this rank's windows fit beside the
+    correction: at most 32 (one stream each) and a small total footprint --
+    otherwise persistent fine windows fill every SM and the correction's
+    chain kernel waits behind whole windows (cfg4 on one GPU: 64 windows of
+    8192 x 256 run phase by phase; on 8 GPUs, 8 per rank, overlapped)."""
+    if not OVERLAP or not isinstance(eng.be, DeviceBackend):
+        return False
+    local = -(-eng.cfg.ng // eng.comm.size)
+    return local <= 32 and local * eng.nx <= 65536
+
+
 class _Overlap:
-    """Single-GPU parareal schedule with the coarse correction overlapped with
-    the fine windows of the next iteration.
+    """Parareal schedule with the coarse correction overlapped with the fine
+    windows of the next iteration, on one GPU or one
+    process per GPU.
 
     F for window n of iteration k+1 needs only row_{k+1}[n-1], which the
     correction of iteration k produces window by window.  So each window's F
@@ -434,10 +460,25 @@ class _Overlap:
     input -- on the window's own stream and solver context (two per window,
     one per iteration parity, so workspaces and status records never mix) --
     and its jump behind the step that produces G(row_{k+1}[n-1]).  The
-    correction runs window by window on its own stream.  Events order all of
-    it; the host reads err (correction stream only) and the statuses of the
-    work it consumed.  Every value is the same function of the same inputs as
-    in the phase-by-phase schedule, so ledgers are bitwise identical; the
+    correction runs window by window on its own stream.  Every window's jump
+    travels as a payload [Delta (nx) | status code, step | kinetic cells]:
+    the status record is stored on the device behind the jump
+    (pk_status_store), so no host synchronisation sits in the pipeline.
+
+    Several ranks: window n of iteration k belongs to rank (n - k - 1) % size
+    (the phase-by-phase deal).  Every rank runs the whole correction itself
+    (deterministic, so all ranks hold the same rows); before correction step
+    n the owner broadcasts window n's payload (NCCL on the correction stream,
+    behind the jump's event), so the correction -- and with it the next
+    iteration's windows on every rank -- advances window by window as the
+    jumps arrive instead of after a whole-iteration all-gather.  Failures
+    travel in the payloads: every rank completes the same collectives and
+    then raises the same error (lowest failing window first, fine before
+    correction, as the reference's order, parareal.py:260-284).
+
+    Events order all of it; the host reads err and the payloads from the
+    correction stream.  Every value is the same function of the same inputs
+    as in the phase-by-phase schedule, so ledgers are bitwise identical; the
     speculative work of an iteration that never happens is dropped unread."""
 
     _cache: dict = {}   # insertion-ordered: least recently used first
@@ -453,7 +494,7 @@ class _Overlap:
 
         key = (_eng.EXACT, id(eng.mesh), str(eng.be.device), cfg.ng, id(cfg.eps), eng.kin_p.dt,
                eng.fluid_p.dt, eng.fluid_p.m2, eng.rtol_f, repr(eng.knobs), tuple(eng.sf),
-               tuple(eng.sc))
+               tuple(eng.sc), eng.comm.size, eng.comm.rank)
         ov = cls._cache.pop(key, None)
         if ov is None or ov.mesh is not eng.mesh or ov.eps is not cfg.eps:
             ov = cls(eng)
@@ -464,13 +505,14 @@ class _Overlap:
         ov.sync()
         ov.clear_status()
         ov.eng = eng
+        ov.comm = eng.comm
         ov.Rn = eng.torch.empty_like(eng.row)
         ov.Gn = eng.torch.empty_like(eng.G)
         return ov
 
     def __init__(self, eng):
         torch = eng.torch
-        self.torch, self.eng = torch, eng
+        self.torch, self.eng, self.comm = torch, eng, eng.comm
         self.mesh, self.eps = eng.mesh, eng.cfg.eps  # keep the key objects alive
         cfg, mesh, be = eng.cfg, eng.mesh, eng.be
         ng, nx, nv = cfg.ng, eng.nx, eng.nv
@@ -480,17 +522,13 @@ class _Overlap:
         self.cdev = Device(mesh, dv)
         # torch hands out streams from a pool of 32 per priority: the
         # correction (the critical path) takes a high-priority stream of its
-        # own; each window one low-priority stream for both parities (windows
-        # beyond 32 share streams, which only serialises them)
+        # own; each window one low-priority stream for both parities
         self.cs = torch.cuda.Stream(dv, priority=-1)
-        # status reads wait on one window's jump event only, not on the
-        # speculative work queued behind it on the window's stream
-        self.ss = torch.cuda.Stream(dv, priority=-1)
         ws = [torch.cuda.Stream(dv) for _ in range(ng)]
         self.fs = [None] + [[s, s] for s in ws]
         f64 = dict(dtype=torch.float64, device=dv)
-        self.D = torch.zeros((2, ng + 1, nx), **f64)           # jumps per parity
-        self.K = torch.zeros((2, ng + 1), dtype=torch.int64, device=dv)
+        # jump payloads per parity: [Delta (nx) | status code, step | kinetic cells]
+        self.D = torch.zeros((2, ng + 1, nx + 3), **f64)
         self.Rn = torch.empty_like(eng.row)                     # next rows
         self.Gn = torch.empty_like(eng.G)                       # next G cache
         self.buf = [None] + [[dict(rho=torch.empty((1, nx), **f64), E=torch.empty((1, nx), **f64),
@@ -524,6 +562,10 @@ class _Overlap:
                         for _ in range(2)]
         self.spec = None    # the iteration whose fine windows are already enqueued
 
+    def owner(self, n, k):
+        """Rank that runs window n in iteration k (the phase-by-phase deal)."""
+        return (n - k - 1) % self.comm.size
+
     def _fine(self, q, n, x_row, wait):
         """Enqueue F for window n (parity q) from x_row [nx] after `wait`."""
         torch, eng = self.torch, self.eng
@@ -541,21 +583,25 @@ class _Overlap:
             dev.fine(b["rho"], b["E"], b["Ep"], b["kc"], b["ki"], b["g"], eng.be.rb1,
                      self.flags[n], None, eng.knobs, [eng.cfg.eps], eng.rtol_f,
                      prepared=self.prep[n][q])
-            self.K[q, n] = b["kc"].sum(dtype=torch.int64)
+            self.D[q, n, eng.nx + 2] = b["kc"].sum(dtype=torch.float64)
 
     def _jump(self, q, n, G_row, wait):
-        """Enqueue Delta = F - G for window n (parity q) after `wait`."""
-        torch = self.torch
-        s = self.fs[n][q]
+        """Enqueue Delta = F - G for window n (parity q) after `wait`, then the
+        window context's status into the payload (re-arming the record)."""
+        torch, nx = self.torch, self.eng.nx
+        s, dev = self.fs[n][q], self.devs[n][q]
         with torch.cuda.stream(s):
             if wait is not None:
                 s.wait_event(wait)
-            self.devs[n][q].jump(self.buf[n][q]["rho"][0], G_row, self.D[q, n])
+            dev.jump(self.buf[n][q]["rho"][0], G_row, self.D[q, n, :nx])
+            dev._rc(dev.lib.pk_status_store(dev.ctx, C.c_void_p(self.D[q, n, nx:].data_ptr()), 1,
+                                            C.c_void_p(s.cuda_stream)), "pk_status_store")
             self.ev_jump[q][n].record(s)
 
     def iterate(self, k):
         torch, eng = self.torch, self.eng
         cfg, ng, nx = eng.cfg, eng.cfg.ng, eng.nx
+        size, rank = self.comm.size, self.comm.rank
         q = k & 1
         self._t_iter = time.perf_counter()
         targets = list(range(k + 1, ng + 1))
@@ -564,8 +610,9 @@ class _Overlap:
         start.record(torch.cuda.current_stream())
         if self.spec != k:   # nothing speculative for this iteration: launch its windows now
             for n in targets:
-                self._fine(q, n, R[n - 1], start)
-                self._jump(q, n, Gc[n], None)
+                if self.owner(n, k) == rank:
+                    self._fine(q, n, R[n - 1], start)
+                    self._jump(q, n, Gc[n], None)
         speculate = k + 1 < cfg.k_max and k + 2 <= ng
         cs, cdev = self.cs, self.cdev
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -576,53 +623,59 @@ class _Overlap:
             c0.record(cs)
         for n in targets:
             with torch.cuda.stream(cs):
-                cs.wait_event(self.ev_jump[q][n])
+                own = self.owner(n, k)
+                if own == rank:
+                    cs.wait_event(self.ev_jump[q][n])
+                if size > 1:
+                    # window n's payload from its owner, in window order on every rank
+                    work = self.comm.broadcast(self.D[q, n], own)
+                    if work is not None:
+                        work.wait()
                 # row_{k+1}[n] = G(row_{k+1}[n-1]) + Delta_k[n]; gout = G(row_{k+1}[n-1])
                 cdev.chain_raw(Rn[n - 1].view(1, nx), Rn[n].view(1, 1, nx), Gn[n].view(1, 1, nx),
-                               None, self.D[q, n].view(1, 1, nx), self.sched[n], eng.fluid_p.dt,
-                               eng.be.rb1, SOLVABILITY_RTOL if eng.rtol is None else eng.rtol)
+                               None, self.D[q, n, :nx].view(1, 1, nx), self.sched[n],
+                               eng.fluid_p.dt, eng.be.rb1,
+                               SOLVABILITY_RTOL if eng.rtol is None else eng.rtol)
                 self.ev_row[n].record(cs)
             if speculate:
-                if n + 1 <= ng:
+                if n + 1 <= ng and self.owner(n + 1, k + 1) == rank:
                     self._fine(q ^ 1, n + 1, Rn[n], self.ev_row[n])
-                if n >= k + 2:
+                if n >= k + 2 and self.owner(n, k + 1) == rank:
                     self._jump(q ^ 1, n, Gn[n], self.ev_row[n])
         with torch.cuda.stream(cs):
             c1.record(cs)
             cdev.maxdiff(Rn, R, eng.be.err_d)
             self.host_enqueue_s = time.perf_counter() - self._t_iter
             err = float(eng.be.err_d.item())     # waits for the correction stream only
+            pay = self.D[q, k + 1:, nx:].cpu().numpy()   # ordered behind every payload
         self.spec = k + 1 if speculate else None
         # the reference raises the fine windows' errors (lowest window first)
         # before any correction error (parareal.py:260-284)
-        for n in targets:
-            self.ss.wait_event(self.ev_jump[q][n])
-            try:
-                self.devs[n][q].check_stream(self.ss)
-            except (SimulationError, ValueError) as ex:
-                raise_for(code_of(ex), f"window {n}, step {getattr(ex, 'pk_step', None)}", n,
-                          getattr(ex, "pk_step", None))
+        for j, n in enumerate(targets):
+            if pay[j, 0] != 0.0:
+                st = int(pay[j, 1])
+                raise_for(int(pay[j, 0]), f"window {n}, step {st}", n, st)
         try:
             cdev.check_stream(cs)
         except SimulationError:
             # one window per launch here: locate the failing window with the
             # phase-by-phase correction (one launch; it raises for that window)
             self.sync()
-            eng.correct(k, self.D[q, k + 1:])
+            eng.correct(k, self.D[q, k + 1:, :nx])
             raise
-        delta = self.D[q, k + 1:].clone()
-        kc = self.K[q].cpu().numpy()
+        delta = self.D[q, k + 1:, :nx].clone()
         fracs = np.zeros(ng + 1)
-        for n in targets:
-            fracs[n] = float(kc[n]) / nx
+        for j, n in enumerate(targets):
+            fracs[n] = float(pay[j, 2]) / nx
         # fine span seen from this iteration's start (speculative windows may
-        # have finished during the previous correction: then ~0)
-        t_fine = max(0.0, max(start.elapsed_time(self.ev_jump[q][n]) for n in targets) * 1e-3)
+        # have finished during the previous correction: then ~0); own windows
+        mine = [n for n in targets if self.owner(n, k) == rank]
+        t_fine = max([0.0] + [start.elapsed_time(self.ev_jump[q][n]) * 1e-3 for n in mine])
         t_corr = c0.elapsed_time(c1) * 1e-3
         if TIMELINE:
             self.timeline = [(n, start.elapsed_time(self.ev_fstart[q][n]),
                               start.elapsed_time(self.ev_jump[q][n]),
-                              start.elapsed_time(self.ev_row[n])) for n in targets]
+                              start.elapsed_time(self.ev_row[n])) for n in mine]
         # swap the row / G buffers: the speculative windows read the new ones
         eng.row, self.Rn = Rn, R
         eng.G, self.Gn = Gn, Gc
@@ -630,8 +683,9 @@ class _Overlap:
 
     def sweep(self):
         """Coarse sweep window by window (parareal.py:210-229; the reference's
-        default field guard), the first iteration's windows enqueued behind the
-        rows they start from, their jumps behind G(row_0[n-1]) == row_0[n]."""
+        default field guard), the first iteration's windows (this rank's)
+        enqueued behind the rows they start from, their jumps behind
+        G(row_0[n-1]) == row_0[n]."""
         torch, eng = self.torch, self.eng
         ng, nx = eng.cfg.ng, eng.nx
         R, Gc, cs = eng.row, eng.G, self.cs
@@ -646,15 +700,16 @@ class _Overlap:
                                     None, None, self.sched[n], eng.fluid_p.dt, eng.be.rb1,
                                     SOLVABILITY_RTOL)
                 self.ev_row[n].record(cs)
-            if eng.cfg.k_max > 0:
+            if eng.cfg.k_max > 0 and self.owner(n, 0) == self.comm.rank:
                 self._fine(0, n, R[n - 1], start if n == 1 else self.ev_row[n - 1])
                 self._jump(0, n, Gc[n], self.ev_row[n])
         self.spec = 0 if eng.cfg.k_max > 0 else None
         self.sweep_enqueue_s = time.perf_counter() - t_host
         self.cdev.check_stream(cs)
         if TIMELINE:
+            mine = [n for n in range(1, ng + 1) if self.owner(n, 0) == self.comm.rank]
             self.sweep_timeline = [(n, start.elapsed_time(self.ev_fstart[0][n]),
-                                    start.elapsed_time(self.ev_row[n])) for n in range(1, ng + 1)]
+                                    start.elapsed_time(self.ev_row[n])) for n in mine]
             self.sweep_wait_s = time.perf_counter() - t_host
 
     def clear_status(self):
@@ -664,6 +719,7 @@ class _Overlap:
         st = _native.PkStatus()
         for d in [self.cdev] + [d for pair in self.devs[1:] for d in pair]:
             d._rc(d.lib.pk_status_read(d.ctx, C.byref(st), 1), "status")
+        self.D.zero_()
 
     def sync(self):
         for pair in self.fs[1:]:
@@ -725,7 +781,7 @@ def coarse_sweep(rho0, cfg: PararealConfig, fluid_p: FluidStepParams, mesh: Phas
     if g0 is None:
         g0 = np.zeros((mesh.nx,) + mesh.vgrid.shape)
     eng = _Engine(cfg, mesh, rho0, g0, rho_bar, fluid_p, kin_p, backend=_BACKEND)
-    if eng.comm.size == 1 and isinstance(eng.be, DeviceBackend) and OVERLAP:
+    if use_overlap(eng):
         eng.overlap = _Overlap.get(eng)
         eng.overlap.sweep()     # also starts iteration 0's windows
     else:

@@ -25,7 +25,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir, which):
+def _worker(rank, world, port, out_dir, which, overlap=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     for p in (ROOT, HERE):
@@ -38,7 +38,10 @@ def _worker(rank, world, port, out_dir, which):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2511_13386_b200 as pk
+        import paper_2511_13386_b200.parareal as ppl
         from paper_2511_13386_b200 import configs
+
+        ppl.OVERLAP = overlap
 
         if which == "cfg2":
             c = configs.cfg2()
@@ -61,10 +64,14 @@ def _worker(rank, world, port, out_dir, which):
         dist.destroy_process_group()
 
 
-def test_cfg2_two_ranks_device_engine(tmp_path, gold):
+@pytest.mark.parametrize("overlap", [True, False], ids=["overlapped", "phase-by-phase"])
+def test_cfg2_two_ranks_device_engine(tmp_path, gold, overlap):
+    """Overlapped: per-window payload broadcasts in window order feed every
+    rank's own correction; phase-by-phase: one all-gather per iteration."""
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), "cfg2"), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), "cfg2", overlap), nprocs=2,
+             join=True)
     d = gold("parareal")
     for r in range(2):
         got = np.load(tmp_path / f"cfg2_{r}.npz")
@@ -73,12 +80,14 @@ def test_cfg2_two_ranks_device_engine(tmp_path, gold):
         assert int(got["meta"][0]) == int(d["c2_meta"][0])
 
 
-def test_cfg3_two_ranks_failure_consensus(tmp_path, gold):
-    """Windows 2..32 all trip the reference guard (fixture); rank 0 holds
+@pytest.mark.parametrize("overlap", [True, False], ids=["overlapped", "phase-by-phase"])
+def test_cfg3_two_ranks_failure_consensus(tmp_path, gold, overlap):
+    """Windows 2..32 all trip the reference guard (fixture); rank 1 holds
     window 2: both ranks must raise window 2's error at the oracle's step."""
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), "cfg3"), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), "cfg3", overlap), nprocs=2,
+             join=True)
     trips = gold("cfg3_iter1")["ref_trip"]
     first = min(n + 1 for n in range(32) if trips[n, 0] >= 0)
     for r in range(2):
