@@ -324,6 +324,139 @@ __device__ bool slice_field_fast(const MeshDev& m, const double* __restrict__ rh
   return true;
 }
 
+// Fast-mode field over EVERY CTA of the cluster (global-memory slice vectors,
+// the hybrid dist slice phase): CTA r takes the r-th contiguous chunk of the
+// cells, its warps contiguous sub-chunks read in coalesced rounds; the CTA
+// partials meet in the leader's shared memory through DSMEM (two cluster
+// barriers), so each pass is nx / (C x warps) cells per warp instead of one
+// CTA walking all of them.  Same arithmetic shape as slice_field_fast.
+__device__ bool cluster_field_fast(const MeshDev& m, const double* __restrict__ rho, double rb,
+                                   double* __restrict__ E_out, double rtol, double* red,
+                                   int rank, int C) {
+  const int nx = m.nx;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int cc = ((nx + C - 1) / C + 31) & ~31;
+  const int clo = min(nx, rank * cc), chi = min(nx, clo + cc);
+  const int cw = ((chi - clo + nw - 1) / nw + 31) & ~31;
+  const int lo = min(chi, clo + warp * cw), hi = min(chi, lo + cw);
+  const double dx = m.dx;
+  double* lred = cg::this_cluster().map_shared_rank(red, 0);   // the leader's scratch
+  auto wsum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(FULL, v, o);
+    return v;
+  };
+  constexpr int U = 4;
+  double ls = 0.0, la = 0.0;
+  for (int b = lo; b < hi; b += 32 * U) {
+    double r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      r[u] = i < hi ? rho[i] : rb;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      ls = ls + (r[u] - rb) * dx;
+      la = la + (i < hi ? fabs(r[u]) : 0.0);
+    }
+  }
+  ls = wsum(ls);
+  la = wsum(la);
+  if (lane == 0) {
+    red[warp] = ls;
+    red[32 + warp] = la;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const double cs_ = wsum(lane < nw ? red[lane] : 0.0);
+    const double ca = wsum(lane < nw ? red[32 + lane] : 0.0);
+    if (lane == 0) {
+      lred[192 + rank] = cs_;
+      lred[208 + rank] = ca;
+    }
+  }
+  cg::this_cluster().sync();
+  const double defect = wsum(lane < C ? lred[192 + lane] : 0.0);
+  const double abssum = wsum(lane < C ? lred[208 + lane] : 0.0);
+  if (fabs(defect) > rtol * fmax(abssum * dx, 2.2250738585072014e-308)) return false;
+  const double corr = defect / (double)nx;
+  double carry = 0.0, part = 0.0;
+  for (int b = lo; b < hi; b += 32 * U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      v[u] = i < hi ? (rho[i] - rb) * dx - corr : 0.0;
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double y = __shfl_up_sync(FULL, v[u], o);
+        if (lane >= o) v[u] = v[u] + y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      const double e = carry + v[u];
+      if (i < hi) {
+        E_out[i] = e;
+        part = part + e;
+      }
+      carry = carry + __shfl_sync(FULL, v[u], 31);
+    }
+  }
+  const double aw = wsum(part);
+  if (lane == 0) {
+    red[64 + warp] = carry;
+    red[96 + warp] = aw;
+    red[128 + warp] = (double)(hi - lo);
+  }
+  __syncthreads();
+  // this CTA's warp offsets, and its partials for the cluster
+  double wi = lane < nw ? red[64 + lane] : 0.0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(FULL, wi, o);
+    if (lane >= o) wi = wi + y;
+  }
+  double we = __shfl_up_sync(FULL, wi, 1);
+  if (lane == 0) we = 0.0;
+  const double woff = __shfl_sync(FULL, we, warp);
+  if (warp == 0) {
+    const double at = wsum(lane < nw ? red[128 + lane] * we + red[96 + lane] : 0.0);
+    if (lane == 31) lred[224 + rank] = wi;            // CTA total
+    if (lane == 0) {
+      lred[240 + rank] = at;                          // sum of the CTA-local prefixes
+      lred[256 + rank] = (double)(chi - clo);         // cells in the CTA
+    }
+  }
+  cg::this_cluster().sync();
+  double ti = lane < C ? lred[224 + lane] : 0.0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(FULL, ti, o);
+    if (lane >= o) ti = ti + y;
+  }
+  double te = __shfl_up_sync(FULL, ti, 1);
+  if (lane == 0) te = 0.0;
+  const double tot = wsum(lane < C ? lred[256 + lane] * te + lred[240 + lane] : 0.0);
+  const double mean = tot / (double)nx;
+  const double off = __shfl_sync(FULL, te, rank) + woff;
+  for (int b = lo; b < hi; b += 32 * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + 32 * u + lane;
+      if (i < hi) E_out[i] = (off + E_out[i]) - mean;
+    }
+  }
+  cg::this_cluster().sync();   // E complete (and the leader's scratch free) everywhere
+  return true;
+}
+
 __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, double* src,
                             double* E_out, double rtol, int exact_scan, bool on_chip,
                             const Smem& sm, long long* dbg = nullptr) {
@@ -939,10 +1072,15 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
   v.Eprev = v.E;
   v.E = t;
   bool ok = true;
-  if (Q.rank == 0)  // the leader CTA solves the field
+  if (Q.dist && !a.exact_scan) {  // fast mode: every CTA of the cluster
+    const long long t0 = (a.prof && v.b == 0 && Q.rank == 0 && tid == 0) ? clock64() : 0;
+    ok = cluster_field_fast(m, v.rho, v.rb, v.E, a.rtol, sm.red, Q.rank, Q.C);
+    if (t0) a.prof[11] += clock64() - t0;
+  } else if (Q.rank == 0) {  // the leader CTA solves the field
     ok = slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, a.local_smem != 0, sm,
                      (a.prof && v.b == 0) ? a.prof + 8 : nullptr);
-  if (Q.dist) {
+  }
+  if (Q.dist && a.exact_scan) {
     if (Q.rank == 0 && tid == 0) Q.flags[42] = ok;
     Q.sync();
     ok = Q.flags[42] != 0;
