@@ -658,6 +658,27 @@ def cfg4_sample(barrier, maxr, peak, ws, fine_steps=100):
                           "coarse_sweep_s": maxr(tm.coarse_sweep),
                           "correction_s": maxr(tm.correction_total),
                           "kinetic_fraction_mean": float(np.mean(res.kinetic_fraction[1:]))})
+                # F alone for one GPU's share at 8 GPUs: 8 lifted windows, one
+                # launch of `fine_steps` steps, kinetic rows counted on the device
+                eng = ppl._Engine(cfg, m, c.rho, c.g, c.rho_bar, fluid_p, kin_p)
+                eng.coarse_sweep()
+                X = eng.row[1:9].clone()
+                cnt = torch.zeros((8, 2), dtype=torch.int64, device=X.device)
+                eng.be.fine(X, list(range(2, 10)))       # warm-up
+                torch.cuda.synchronize()
+                eng.be.dev.count_rows(cnt)
+                e4, e5 = _event(), _event()
+                e4.record()
+                eng.be.fine(X, list(range(2, 10)))
+                e5.record()
+                torch.cuda.synchronize()
+                eng.be.dev.count_rows(None)
+                f8 = e4.elapsed_time(e5) * 1e-3
+                rows, zrows = (int(v) for v in cnt.sum(dim=0).tolist())
+                alg = 16 * m.nv * rows + 8 * m.nv * zrows
+                r.update({"fine_us_per_step_8_windows": f8 / fine_steps * 1e6,
+                          "kinetic_fraction_of_updates_8_windows": rows / (8 * fine_steps * m.nx),
+                          "hbm_frac_8_windows": alg / f8 / (peak * 1e9)})
                 # G alone: one coarse chain of `csteps` steps per window on one GPU
                 dev = pk.engine.Device.for_mesh(m)
                 rho_d = dev.t(np.ascontiguousarray(c.rho.reshape(1, -1)))
@@ -676,9 +697,11 @@ def cfg4_sample(barrier, maxr, peak, ws, fine_steps=100):
                 fine_step = fine_s / fine_steps
                 r.update({"coarse_us_per_step": coarse_step * 1e6,
                           "fine_us_per_step_all_local_windows": fine_step * 1e6,
-                          "extrapolated_full_T_iteration_s": fine_step * full_steps
-                          + coarse_step * full_csteps * ng,
-                          "extrapolated_full_T_coarse_sweep_s": coarse_step * full_csteps * ng})
+                          "extrapolated_full_T_coarse_sweep_s": coarse_step * full_csteps * ng,
+                          # one iteration at full T on 8 GPUs, phase by phase:
+                          # 8 windows of F per GPU, then the 64-window correction
+                          "extrapolated_full_T_iteration_s_8gpu_phase_by_phase":
+                              f8 / fine_steps * full_steps + coarse_step * full_csteps * ng})
             except pk.SimulationError as ex:
                 r["status"] = f"raised {type(ex).__name__} ({ex})"
         out["exact" if exact else "fast_mode"] = r

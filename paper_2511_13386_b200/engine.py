@@ -112,6 +112,27 @@ def per_value(values: np.ndarray, fn) -> np.ndarray:
     return out
 
 
+_COEF_ROWS: dict = {}   # (mesh, eps, dt) -> coefficient rows (insertion-ordered LRU)
+
+
+def _coef_rows(mesh: PhaseMesh, eps, dt: float):
+    """kappa1, kappa2 and dt/(eps dx) per interface for one (eps, dt): Python
+    floats per distinct eps value (an eps(x) profile has nx of them, ~30 ms
+    at nx = 8192), so they are cached across calls."""
+    key = (id(mesh), id(eps) if hasattr(eps, "iface") else float(eps), dt)
+    hit = _COEF_ROWS.pop(key, None)
+    if hit is None or hit[0] is not mesh or (hasattr(eps, "iface") and hit[1] is not eps):
+        e = eps_rows(eps, mesh.nx)
+        dx = mesh.dx
+        hit = (mesh, eps, (per_value(e, lambda v: relaxation_coefficients(dt, v)[0]),
+                           per_value(e, lambda v: relaxation_coefficients(dt, v)[1]),
+                           per_value(e, lambda v: dt / (v * dx))))
+    _COEF_ROWS[key] = hit
+    while len(_COEF_ROWS) > 64:
+        _COEF_ROWS.pop(next(iter(_COEF_ROWS)))
+    return hit[2]
+
+
 def make_phase(mesh: PhaseMesh, eps_list, dt_list, nsteps_list) -> Phase:
     """Coefficients of a run of steps; slice b uses eps_list[b], dt_list[b]."""
     B = len(eps_list)
@@ -121,18 +142,10 @@ def make_phase(mesh: PhaseMesh, eps_list, dt_list, nsteps_list) -> Phase:
     cm = np.empty((B, nx))
     cflu = np.empty(B)
     dts = np.empty(B)
-    rows = {}  # slices sharing (eps, dt) share their coefficient rows
     for b in range(B):
         dt = float(dt_list[b])
         dts[b] = dt
-        eb = eps_list[b]
-        key = (id(eb) if hasattr(eb, "iface") else float(eb), dt)
-        if key not in rows:
-            e = eps_rows(eb, nx)
-            rows[key] = (per_value(e, lambda v: relaxation_coefficients(dt, v)[0]),
-                         per_value(e, lambda v: relaxation_coefficients(dt, v)[1]),
-                         per_value(e, lambda v: dt / (v * dx)))
-        k1[b], k2[b], cm[b] = rows[key]
+        k1[b], k2[b], cm[b] = _coef_rows(mesh, eps_list[b], dt)
         cflu[b] = m2 * (dt / dx)
     def uniform(a):  # per slice: the common value of a row, else NaN
         return np.array([row[0] if (row == row[0]).all() else np.nan for row in a])
