@@ -410,7 +410,13 @@ class _Engine:
                     Fall[n - k - 1] = part[j]
                     kcount[n - k - 1] = part[per, j].to(torch.int64)
         t1 = be.clock()
-        delta = be.jump(Fall, self.G[k + 1:])   # NonFiniteState (parareal.py:267-269)
+        try:
+            delta = be.jump(Fall, self.G[k + 1:])   # NonFiniteState (parareal.py:267-269)
+        except NonFiniteState:
+            # name the lowest non-finite window, as the reference's message does
+            bad = (~torch.isfinite(Fall - self.G[k + 1:])).any(dim=1).nonzero()
+            n = targets[int(bad[0, 0])] if bad.numel() else targets[0]
+            raise NonFiniteState(f"non-finite fine/coarse jump in window {n} (blow-up)") from None
         t2 = be.clock()
         new = self.row.clone()
         Gn = self.G.clone()
