@@ -40,6 +40,17 @@ def main(rep, out, title, alg=None):
     with open(out, "w") as f:
         f.write(f"# {title}\n# kernel: {get('Kernel Name')}\n# report: {os.path.basename(rep)} "
                 f"({len(rr) - 2} profiled launch(es); first shown)\n\n")
+        if len(rr) > 3:
+            f.write("# all profiled launches: kernel | duration | registers | issue active % | "
+                    "FP64 pipe % | DRAM bytes r+w\n")
+            for row in rr[2:]:
+                g = lambda k: row[H.index(k)] if k in H else "-"  # noqa: E731
+                f.write(f"#   {g('Kernel Name')[:60]:60s} | {g('gpu__time_duration.sum')} "
+                        f"{U[H.index('gpu__time_duration.sum')]} | {g('launch__registers_per_thread')}"
+                        f" | {g('smsp__issue_active.avg.pct_of_peak_sustained_active')} | "
+                        f"{g('sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active')} | "
+                        f"{g('dram__bytes_read.sum')}+{g('dram__bytes_write.sum')}\n")
+            f.write("\n")
         for k in KEYS:
             if k in H:
                 f.write(f"{k:75s} {U[H.index(k)]:12s} {V[H.index(k)]}\n")
