@@ -433,18 +433,27 @@ def main():
     extra = {}
     if not args.no_extras:
         # collectives: every rank runs the engine (windows dealt across ranks)
-        par, gpu_rows = parareal_cfg2(barrier, maxr, peak)
-        c4 = cfg4_sample(barrier, maxr, peak, ws)
-        c3 = cfg3_iteration1(barrier, peak)   # run() is collective: every rank
-        c5f = cfg5_fast(ens_args=(m, eps, dts, rb, rho_d, g_d, upd_rank), barrier=barrier,
-                        maxr=maxr, peak=peak, ws=ws)
+        def guarded(fn, *a, **kw):
+            # an extra that fails (on every rank alike) is reported, not fatal:
+            # the headline line must still print
+            try:
+                return fn(*a, **kw)
+            except Exception as ex:  # noqa: BLE001
+                return {"error": f"{type(ex).__name__}: {ex}"[:400]}
+
+        par = guarded(parareal_cfg2, barrier, maxr, peak)
+        gpu_rows = par.pop("_rows", None)
+        c4 = guarded(cfg4_sample, barrier, maxr, peak, ws)
+        c3 = guarded(cfg3_iteration1, barrier, peak)   # run() is collective: every rank
+        c5f = guarded(cfg5_fast, ens_args=(m, eps, dts, rb, rho_d, g_d, upd_rank),
+                      barrier=barrier, maxr=maxr, peak=peak, ws=ws)
         barrier()
         if rank == 0:
             extra["parareal"] = par
             extra["cfg4"] = c4
             extra["cfg3"] = c3
             extra["cfg5_fast_mode"] = c5f
-            extra["v3"] = v3_default_grid(peak)
+            extra["v3"] = guarded(v3_default_grid, peak)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "fine_kernel_traffic.json")
     if os.path.exists(tpath):
@@ -456,7 +465,7 @@ def main():
     if rank == 0 and not args.no_cpu:
         pool = CpuPool()
         cpu = pool.cfg5()
-        if "parareal" in extra:
+        if "parareal" in extra and gpu_rows is not None:
             cpar, crows = pool.cfg2_parareal()
             cpar["gpu_ledger_bitwise_equal"] = bool(
                 len(crows) == len(gpu_rows) and all(np.array_equal(a, b)
@@ -563,7 +572,8 @@ def parareal_cfg2(barrier, maxr, peak):
             rows = [np.asarray(x) for x in res.ledger.rho]
         else:
             out["fast_mode"] = r
-    return out, rows
+    out["_rows"] = rows
+    return out
 
 
 def cfg3_iteration1(barrier, peak):
