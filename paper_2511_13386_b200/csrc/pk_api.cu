@@ -224,12 +224,18 @@ pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   m.dx = mesh->dx;
   m.rdx = 1.0 / mesh->dx;
   m.two_dx = 2.0 * mesh->dx;
+  m.rtwo_dx = 1.0 / m.two_dx;
+  m.rdvx = 1.0 / mesh->dvx;
   m.dvx = mesh->dvx;
   m.dv3 = mesh->dv3;
   m.m0 = mesh->m0;
   m.m2 = mesh->m2;
   std::memcpy(m.stc, mesh->stencil, sizeof(m.stc));
   std::memcpy(m.sts, mesh->stencil_scale, sizeof(m.sts));
+  m.stc_std = 1;
+  for (int p = 0; p < 4; ++p)
+    for (int o = 0; o < 7; ++o)
+      if ((m.stc[p][o] == 0.0) != ((p == 0 || p == 2) && o == 3)) m.stc_std = 0;
   std::vector<double> h(4 * (size_t)nv);
   std::memcpy(h.data(), mesh->vx, nv * 8);
   std::memcpy(h.data() + nv, mesh->M, nv * 8);

@@ -16,6 +16,9 @@ struct MeshDev {
   int mirror;          // vx[nv-1-j] == -vx[j], M[nv-1-j] == M[j] and xiM[j] == vx[j]*M[j]
                        // bit for bit (the reference's mirrored grid, mesh.py:31-44,136)
   double dx, rdx, two_dx, dvx, dv3, m0, m2;
+  double rtwo_dx, rdvx;  // RN(1 / (2 dx)), RN(1 / dvx): qdiv's reciprocals
+  int stc_std;         // the stencil table has the reference's zero pattern (only
+                       // orders 1 and 3 have a zero, at offset 0): skip statically
   double three_rb_unused;
   const double* vx;    // [nv] velocity centres xi_j
   const double* M;     // [nv] discrete Maxwellian

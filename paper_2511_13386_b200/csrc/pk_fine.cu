@@ -208,9 +208,17 @@ __device__ __forceinline__ double stencil_at(const double* v, int i, int nx, con
   return acc * m.sts[p - 1];
 }
 
-// stencil_at on a register window w[o] = v[i + o - 3] (same terms, same order)
+// stencil_at on a register window w[o] = v[i + o - 3] (same terms, same order).
+// With the reference's table (m.stc_std) the zero terms it skips are known:
+// the offset-0 term of orders 1 and 3 -- no per-term test.
 __device__ __forceinline__ double stencil_reg(const double (&w)[7], const MeshDev& m, int p) {
   double acc = 0.0;
+  if (m.stc_std) {
+#pragma unroll
+    for (int o = 0; o < 7; ++o)
+      if (!((p == 1 || p == 3) && o == 3)) acc = acc + m.stc[p - 1][o] * w[o];
+    return acc * m.sts[p - 1];
+  }
 #pragma unroll
   for (int o = 0; o < 7; ++o) {
     const double c = m.stc[p - 1][o];
@@ -685,9 +693,9 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       const double J = flux_J(v.rho[i], v.rho[in_], e, m.dx, m.rdx);
       v.J[i] = J;
       v.gJ[i] = J;
-      v.dco[i] = (v.fl[in_] - v.fl[ip]) / m.two_dx;
+      v.dco[i] = qdiv(v.fl[in_] - v.fl[ip], m.two_dx, m.rtwo_dx);
       v.vsg[i] = e > 0.0 ? 1 : (e < 0.0 ? -1 : 0);
-      v.vco[i] = e / m.dvx;
+      v.vco[i] = qdiv(e, m.dvx, m.rdvx);
     }
     if (tid == 0) *v.nk = nx;
     __syncthreads();
@@ -736,6 +744,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   PK_PTICK(0)
   // remainder indicator (adaptation.py:120-152) at cells
   {
+    const double rdt = 1.0 / dt;   // qdiv's reciprocal for (E - E_prev) / dt
     constexpr int U = 4;
     for (int i0 = P.r0; i0 < nx; i0 += U * P.rs) {
       double e[U], ep[U], j0[U], j1[U];
@@ -751,7 +760,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
       for (int u = 0; u < U; ++u) {
         const int i = i0 + u * P.rs;
         if (i < nx) {
-          tA_[i] = (e[u] - ep[u]) / dt;  // (E - E_prev)/dt
+          tA_[i] = qdiv(e[u] - ep[u], dt, rdt);  // (E - E_prev)/dt
           tB_[i] = 0.5 * (j0[u] + j1[u]);  // J_c
         }
       }
@@ -981,9 +990,9 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
         const int i = i00 + u * P.rs + P.r0;
         bool z = false;
         if (i < nx) {
-          dco_[i] = (b1[u] - b0[u]) / m.two_dx;
+          dco_[i] = qdiv(b1[u] - b0[u], m.two_dx, m.rtwo_dx);
           vsg_[i] = e[u] > 0.0 ? 1 : (e[u] < 0.0 ? -1 : 0);
-          vco_[i] = e[u] / m.dvx;
+          vco_[i] = qdiv(e[u], m.dvx, m.rdvx);
           z = !k[u] && nz[u];
           if (z) nzo[i] = 0;
         }
