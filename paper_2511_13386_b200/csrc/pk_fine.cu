@@ -467,7 +467,7 @@ __device__ bool cluster_field_fast(const MeshDev& m, const double* __restrict__ 
 
 __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, double* src,
                             double* E_out, double rtol, int exact_scan, bool on_chip,
-                            const Smem& sm, long long* dbg = nullptr) {
+                            const Smem& sm, long long* dbg = nullptr, bool src_ready = false) {
   const int nx = m.nx;
   long long c0 = dbg ? clock64() : 0;
 #define PK_TICK(k)                         \
@@ -530,8 +530,10 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
     PK_TICK(5)
     return true;
   }
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = (rho[i] - rb) * m.dx;
-  __syncthreads();
+  if (!src_ready) {  // (finish_step forms src in its rho-update pass)
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = (rho[i] - rb) * m.dx;
+    __syncthreads();
+  }
   PK_TICK(0)
   double defect, abssum;
   block_pairwise2([&](int i) { return src[i]; }, [&](int i) { return fabs(rho[i]); }, *sm.plan,
@@ -1059,6 +1061,12 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
   const size_t o = (size_t)v.b * nx;
   const double cflu = P.cflu[v.b];
   const double cs = P.cmacs ? P.cmacs[v.b] : __longlong_as_double(0x7ff8000000000000LL);
+  // the exact field's source (rho' - rho_bar) dx is formed here, into the
+  // buffer the field is solved in (the outgoing E_prev, rotated below), when
+  // the leader solves on that buffer (slice_field's generic path)
+  const bool pre_src = a.exact_scan && !Q.dist && !(sm.scan && a.local_smem == 0);
+  double* const src = v.Eprev;
+  const double rb = v.rb, dx = m.dx;
   for (int i = Q.r0; i < nx; i += Q.rs) {
     const int ip = wrap(i - 1, nx);
     const double rho = v.rho[i];
@@ -1073,6 +1081,7 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
       r = rho + cflu * (v.J[i] - v.J[ip]);
     }
     v.rho[i] = r;  // in place: each rho_i update reads only its own rho_i
+    if (pre_src) src[i] = (r - rb) * dx;
   }
   Q.sync();
   // the new field is solved in place in the E_prev buffer; the old E becomes
@@ -1087,7 +1096,7 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
     if (t0) a.prof[11] += clock64() - t0;
   } else if (Q.rank == 0) {  // the leader CTA solves the field
     ok = slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, a.local_smem != 0, sm,
-                     (a.prof && v.b == 0) ? a.prof + 8 : nullptr);
+                     (a.prof && v.b == 0) ? a.prof + 8 : nullptr, pre_src);
   }
   if (Q.dist && a.exact_scan) {
     if (Q.rank == 0 && tid == 0) Q.flags[42] = ok;
