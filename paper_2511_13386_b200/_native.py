@@ -14,7 +14,8 @@ import os
 from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpk.so")
+# PK_LIB_PATH: load another build of the same ABI (A/B measurements only)
+LIB_PATH = os.environ.get("PK_LIB_PATH") or os.path.join(_HERE, "libpk.so")
 
 c_double_p = C.POINTER(C.c_double)
 c_int32_p = C.POINTER(C.c_int32)

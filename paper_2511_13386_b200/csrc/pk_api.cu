@@ -116,6 +116,19 @@ bool build_plan(int n, PwPlan* P) {
       if (pb.nodes[order[i]].level <= lev) end = i + 1;
     P->level_end[lev - 1] = end;
   }
+  // perfect: 2^L leaves and level l's q-th node adds items 2q, 2q+1 of level
+  // l-1 (the leaves at level 0) -- the xor-butterfly form (pw_perfect)
+  bool perf = (nleaf & (nleaf - 1)) == 0 && (1 << maxlev) == nleaf;
+  int prev0 = 0, start = 0;  // first operand index of level l-1, first node of level l
+  for (int lev = 1; perf && lev <= maxlev; ++lev) {
+    const int end = P->level_end[lev - 1];
+    if (end - start != nleaf >> lev) perf = false;
+    for (int q = 0; perf && q < end - start; ++q)
+      perf = P->node_a[start + q] == prev0 + 2 * q && P->node_b[start + q] == prev0 + 2 * q + 1;
+    prev0 = nleaf + start;
+    start = end;
+  }
+  P->perfect = perf ? 1 : 0;
   return true;
 }
 

@@ -50,6 +50,7 @@ struct PwPlan {
   int node_a[MAX_NODE];      // operand indices into vals[nleaf + nnode]
   int node_b[MAX_NODE];
   int level_end[MAX_LEVEL];  // nodes [level_end[l-1], level_end[l]) form level l
+  int perfect;               // 2^L leaves combined as adjacent pairs level by level
 };
 
 // One pairwise leaf (n <= 128) over x[off .. off+n) computed by a whole warp;
@@ -280,6 +281,86 @@ __device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int 
   }
 }
 
+// Pairwise sums over a PERFECT plan (P.perfect: 2^L leaves, combined as
+// adjacent pairs level by level -- every nx = 2^k x (<= 128)): one leaf per
+// 8-lane group (group_leaf), the tree by xor butterflies.  a + b == b + a
+// bitwise, so the butterfly's lane order gives numpy's node values exactly.
+// NS sums of the same plan (x(s, i), s < NS); every thread gets the results.
+// NS nleaf <= 4: every warp sums all the leaves itself -- no shared memory,
+// no barrier.  Else the leaves are dealt over the warps, the 4-leaf subtrees
+// meet in `scr` (NS nleaf / 4 doubles) behind ONE barrier and every warp
+// finishes the tree itself; the caller keeps a barrier between this call's
+// reads of scr and the next writes to it.
+template <int NS, class F>
+__device__ __forceinline__ void pw_perfect(F x, const PwPlan& P, double* scr, double (&res)[NS]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int nl = P.nleaf, ntask = NS * nl;
+  if (ntask <= 4) {
+    const int t = lane >> 3;
+    const bool act = t < ntask;
+    const int s = act ? t / nl : 0, l = act ? t - s * nl : 0;
+    double v = group_leaf([&](int i) { return x(s, i); }, act ? P.leaf_off[l] : 0,
+                          act ? P.leaf_len[l] : 0, act);
+    if (nl >= 2) v = v + __shfl_xor_sync(FULL, v, 8);
+    if (nl >= 4) v = v + __shfl_xor_sync(FULL, v, 16);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) res[q] = __shfl_sync(FULL, v, 8 * nl * q);
+    return;
+  }
+  // nl >= 4 here (a power of two): aligned groups of four leaves share a sum
+  for (int t0 = 4 * warp; t0 < ntask; t0 += 4 * nwarp) {
+    const int t = t0 + (lane >> 3);
+    const int s = t / nl, l = t - s * nl;
+    double v = group_leaf([&](int i) { return x(s, i); }, P.leaf_off[l], P.leaf_len[l], true);
+    v = v + __shfl_xor_sync(FULL, v, 8);
+    v = v + __shfl_xor_sync(FULL, v, 16);
+    if (lane == 0) scr[t0 >> 2] = v;
+  }
+  __syncthreads();
+  const int nsub = nl >> 2;  // <= 16 (MAX_LEAF)
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    double w = lane < nsub ? scr[q * nsub + lane] : 0.0;
+    for (int o = 1; o < nsub; o <<= 1) w = w + __shfl_xor_sync(FULL, w, o);
+    res[q] = __shfl_sync(FULL, w, 0);
+  }
+}
+
+// Exact field (poisson.py:41-54) of a slice whose vectors are in shared
+// memory: pairwise defect and sum|rho| (pw_perfect when the plan is perfect,
+// else block_pairwise2), the guard, x - defect/nx, the sequential np.cumsum
+// chain on thread 0, the pairwise mean.  Same operations in the same order
+// as slice_field's generic path, same bits.
+//   x:  in  (rho - rho_bar) dx for every cell (the caller's barrier done),
+//       out the running sums E + mean (in place)
+//   mean: E = x - mean is left to the caller (x - 0.0 == x: a pending shift
+//       of 0 is exact)
+// `red`: 2 (nleaf + nnode) doubles.  Returns false on a solvability
+// violation (uniform over the block).
+template <class FA>
+__device__ bool field_exact_onchip(FA absrho, double* x, int nx, double dx, double rtol,
+                                   const PwPlan& P, double* red, double& mean) {
+  double r[2];
+  if (P.perfect)
+    pw_perfect<2>([&](int s, int i) { return s ? absrho(i) : x[i]; }, P, red, r);
+  else
+    block_pairwise2([&](int i) { return x[i]; }, absrho, P, red, r[0], r[1]);
+  if (fabs(r[0]) > rtol * fmax(r[1] * dx, 2.2250738585072014e-308)) return false;
+  const double corr = r[0] / (double)nx;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) x[i] = x[i] - corr;
+  __syncthreads();
+  smem_cumsum(x, x, nx);
+  __syncthreads();
+  if (P.perfect) {
+    double mm[1];
+    pw_perfect<1>([&](int, int i) { return x[i]; }, P, red, mm);
+    mean = mm[0] / (double)nx;
+  } else {
+    mean = block_pairwise([&](int i) { return x[i]; }, P, red) / (double)nx;
+  }
+  return true;
+}
+
 // Work-efficient parallel prefix sum (fast mode, not bitwise): block scan with
 // warp shuffles over a blocked partition.  `scratch` holds blockDim.x/32 + 1
 // doubles.  Result differs from np.cumsum by O(n u |E|).
@@ -315,6 +396,12 @@ __device__ void block_scan_fast(FS src, FD dst, int n, double* scratch) {
     dst(i, run);
   }
   __syncthreads();
+}
+
+// profiling counters: a fire-and-forget reduction (no load round trip on
+// the profiled thread's timeline)
+__device__ __forceinline__ void pk_red_add(long long* p, long long v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
 __device__ __forceinline__ int wrap(int i, int n) {

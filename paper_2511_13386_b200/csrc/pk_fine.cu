@@ -104,6 +104,9 @@ struct SliceView {
   double* ga;
   double* gb;
   double rb;
+  // exact on-chip field: E = E[i] - Emean is still to be applied (Epend)
+  double Emean;
+  bool Epend;
 };
 
 // number of leader-local double / byte vectors (all-kinetic mode needs the
@@ -133,6 +136,8 @@ __device__ __forceinline__ void bind_shared(SliceView& v, const FineArgs& a, int
   v.ga = a.ga + o * a.m.nv;
   v.gb = a.gb + o * a.m.nv;
   v.rb = a.rho_bar[b];
+  v.Emean = 0.0;
+  v.Epend = false;
 }
 
 // Leader-local vectors either in shared memory (loc != null: the same smem
@@ -467,13 +472,14 @@ __device__ bool cluster_field_fast(const MeshDev& m, const double* __restrict__ 
 
 __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, double* src,
                             double* E_out, double rtol, int exact_scan, bool on_chip,
-                            const Smem& sm, long long* dbg = nullptr, bool src_ready = false) {
+                            const Smem& sm, long long* dbg = nullptr, bool src_ready = false,
+                            double* mean_out = nullptr) {
   const int nx = m.nx;
   long long c0 = dbg ? clock64() : 0;
 #define PK_TICK(k)                         \
   if (dbg && threadIdx.x == 0) {           \
     const long long c1 = clock64();        \
-    dbg[k] += c1 - c0;                     \
+    pk_red_add(dbg + k, c1 - c0);          \
     c0 = c1;                               \
   }
   if (!exact_scan) {
@@ -510,15 +516,15 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
       return true;
     }
     double carry = -0.0;  // np.cumsum's chain starts from the first operand
-    for (int c0 = 0; c0 < nx; c0 += sm.scan_cap) {
-      const int len = min(sm.scan_cap, nx - c0);
+    for (int q0 = 0; q0 < nx; q0 += sm.scan_cap) {
+      const int len = min(sm.scan_cap, nx - q0);
       for (int i = threadIdx.x; i < len; i += blockDim.x)
-        sc[i] = (rho[c0 + i] - rb) * m.dx - corr;
+        sc[i] = (rho[q0 + i] - rb) * m.dx - corr;
       __syncthreads();
       smem_cumsum(sc, sc, len, carry);
       __syncthreads();
       carry = sc[len - 1];
-      for (int i = threadIdx.x; i < len; i += blockDim.x) E_out[c0 + i] = sc[i];
+      for (int i = threadIdx.x; i < len; i += blockDim.x) E_out[q0 + i] = sc[i];
       __syncthreads();
     }
     PK_TICK(3)
@@ -533,6 +539,27 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
   if (!src_ready) {  // (finish_step forms src in its rho-update pass)
     for (int i = threadIdx.x; i < nx; i += blockDim.x) src[i] = (rho[i] - rb) * m.dx;
     __syncthreads();
+  }
+  if (on_chip) {
+    // vectors on chip: field_exact_onchip, in place on E_out
+    if (src != E_out) {
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) E_out[i] = src[i];
+      __syncthreads();
+    }
+    PK_TICK(0)
+    double mean;
+    if (!field_exact_onchip([&](int i) { return fabs(rho[i]); }, E_out, nx, m.dx, rtol, *sm.plan,
+                            sm.red, mean))
+      return false;
+    PK_TICK(3)
+    if (mean_out) {  // the caller applies E - mean where it next reads E
+      *mean_out = mean;
+    } else {
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) E_out[i] = E_out[i] - mean;
+      __syncthreads();
+    }
+    PK_TICK(5)
+    return true;
   }
   PK_TICK(0)
   double defect, abssum;
@@ -675,7 +702,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
 #define PK_PTICK(k)                        \
   if (dbg && threadIdx.x == 0) {           \
     const long long c1 = clock64();        \
-    dbg[k] += c1 - c0;                     \
+    pk_red_add(dbg + k, c1 - c0);          \
     c0 = c1;                               \
   }
   const MeshDev& m = a.m;
@@ -687,11 +714,13 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   if constexpr (!AD) {
     // all-kinetic: J, and the projection/E-upwind coefficients from the
     // unmasked moments (kinetic.py:177-178,190-191,221)
+    const double Em = v.Emean;  // pending zero-mean shift of E (0.0: none)
     for (int i = tid; i < nx; i += nt) {
       const int in_ = wrap(i + 1, nx), ip = wrap(i - 1, nx);
       v.kc[i] = 1;  // adaptation off: all kinetic (hybrid.py:167-168)
       v.ki[i] = 1;
-      const double e = v.E[i];
+      const double e = v.E[i] - Em;
+      if (v.Epend) v.E[i] = e;
       const double J = flux_J(v.rho[i], v.rho[in_], e, m.dx, m.rdx);
       v.J[i] = J;
       v.gJ[i] = J;
@@ -709,7 +738,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   // unconditionally first (restrict views, no load behind a branch), so the
   // L2 round trips of consecutive iterations overlap.
   const double* __restrict__ rho_ = v.rho;
-  const double* __restrict__ E_ = v.E;
+  double* __restrict__ E_ = v.E;
   const double* __restrict__ Ep_ = v.Eprev;
   double* __restrict__ J_ = v.J;
   double* __restrict__ gJ_ = v.gJ;
@@ -724,12 +753,13 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
         const int i = min(i0 + u * P.rs, nx - 1);
         r0[u] = rho_[i];
         r1[u] = rho_[wrap(i + 1, nx)];
-        e[u] = E_[i];
+        e[u] = E_[i] - v.Emean;  // the pending zero-mean shift (0.0: none)
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i = i0 + u * P.rs;
         if (i < nx) {
+          if (v.Epend) E_[i] = e[u];
           const double J = flux_J(r0[u], r1[u], e[u], m.dx, m.rdx);
           J_[i] = J;
           gJ_[i] = J;
@@ -869,7 +899,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   P.sync();
   PK_PTICK(2)
   const int nflip = sflags[40];
-  if (dbg && tid == 0) dbg[10] += nflip;
+  if (dbg && tid == 0) pk_red_add(dbg + 10, nflip);
   if (sflags[0]) {
     if (a.reinit == 0) {
       if (a.lift_order != 1 && a.lift_order != 2) {
@@ -885,7 +915,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
         const int i = v.klist[q];
         const int in_ = wrap(i + 1, nx);
         const double dJ = 0.5 * (v.tD[i] + v.tD[in_]);
-        v.tE[i] = dJ - v.E[i] * v.J[i];          // drift
+        v.tE[i] = dJ - E_[i] * v.J[i];           // drift
         v.tA[i] = 0.5 * (v.tC[i] + v.tC[in_]);   // R_if
       }
       P.sync();
@@ -1008,7 +1038,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   PK_PTICK(5)
   if (P.rank == 0 && tid == 0) {
     *v.nzl = sflags[41];
-    if (dbg) dbg[11] += sflags[41];
+    if (dbg) pk_red_add(dbg + 11, sflags[41]);
   }
   PK_PTICK(6)
   // compacted kinetic-row list (order preserving: contiguous chunks per
@@ -1022,7 +1052,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
   for (int i = lo; i < hi; ++i)
     if (v.ki[i]) v.klist[pre++] = i;
   if (P.rank == 0 && tid == 0) *v.nk = total;
-  if (dbg && tid == 0) dbg[12] += total;
+  if (dbg && tid == 0) pk_red_add(dbg + 12, total);
   P.sync();
   PK_PTICK(7)
   // row-stream positions for the producer/consumer micro phase: entry p needs
@@ -1093,10 +1123,16 @@ __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int
   if (Q.dist && !a.exact_scan) {  // fast mode: every CTA of the cluster
     const long long t0 = (a.prof && v.b == 0 && Q.rank == 0 && tid == 0) ? clock64() : 0;
     ok = cluster_field_fast(m, v.rho, v.rb, v.E, a.rtol, sm.red, Q.rank, Q.C);
-    if (t0) a.prof[11] += clock64() - t0;
+    if (t0) pk_red_add(a.prof + 11, clock64() - t0);
   } else if (Q.rank == 0) {  // the leader CTA solves the field
+    // on chip, exact: the zero-mean shift stays pending (v.Emean) until the
+    // next prepare_step's first pass (or the end of the window) applies it
+    const bool pend = a.exact_scan && a.local_smem != 0 && !Q.dist;
     ok = slice_field(m, v.rho, v.rb, v.E, v.E, a.rtol, a.exact_scan, a.local_smem != 0, sm,
-                     (a.prof && v.b == 0) ? a.prof + 8 : nullptr, pre_src);
+                     (a.prof && v.b == 0) ? a.prof + 8 : nullptr, pre_src,
+                     pend ? &v.Emean : nullptr);
+    v.Epend = pend && ok;
+    if (!v.Epend) v.Emean = 0.0;
   }
   if (Q.dist && a.exact_scan) {
     if (Q.rank == 0 && tid == 0) Q.flags[42] = ok;
@@ -2571,6 +2607,11 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
   // optional row counters (pk_count_rows): the slice owner's thread 0
   const bool rcnt = a.rowcnt && leader && threadIdx.x == 0;
   long long rc_rows = 0, rc_zero = 0;
+  if (a.stagger > 0) {  // experiment: desynchronise the software groups' steps
+    const long long d = (long long)((blockIdx.x / (unsigned)C) % (unsigned)a.stagger_mod) * a.stagger;
+    const long long t0 = clock64();
+    while (clock64() - t0 < d) __nanosleep(256);
+  }
   for (int s = 0; s < nst_all; ++s) {
     const int ph = s < n0 ? 0 : 1;
     if constexpr (AD) {  // rows the slice phase listed for zeroing in this step's output
@@ -2637,7 +2678,12 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
         const int phn = (s + 1) < n0 ? 0 : 1;
         ok = prepare_step<T, AD>(a, v, sm, a.ph[phn].dt[b], 0, buf(s + 1), nzf(s + 1), nzf(s),
                                  s + 1, par, (a.prof && b == 0 && leader) ? a.prof + 16 : nullptr);
+      } else if (ok && v.Epend) {  // last step: the field's pending zero-mean shift
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) v.E[i] = v.E[i] - v.Emean;
+        __syncthreads();
       }
+      v.Epend = false;
+      v.Emean = 0.0;
       if (!ok && threadIdx.x == 0) *abort_flag = 1;
       if (prof) { c1 = clock64(); tp[3] += c1 - c0; c0 = c1; }
     }
@@ -2944,6 +2990,12 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
     }
   }
   const bool sg = a.sg > 1;
+  {
+    static const long long stg = getenv("PK_SG_STAGGER") ? atoll(getenv("PK_SG_STAGGER")) : 0;
+    static const int stm = getenv("PK_SG_STAGGER_MOD") ? atoi(getenv("PK_SG_STAGGER_MOD")) : 2;
+    a.stagger = sg ? stg : 0;
+    a.stagger_mod = stm > 0 ? stm : 2;
+  }
   if (dbg_packing)
     fprintf(stderr, "pk packing: B %d, %s of %d CTAs x %d slices\n", a.B,
             a.sg > 1 ? "software group" : "cluster", C, a.kps);

@@ -14,7 +14,7 @@ struct Smem {
   double* xiM;
   double* w2;
   PwPlan* plan;
-  double* red;    // pairwise scratch (MAX_LEAF + MAX_NODE)
+  double* red;    // pairwise scratch (2 (MAX_LEAF + MAX_NODE))
   double* wrow;   // generic rows: one nv-row per warp
   int* misc;      // small ints
   double* scan = nullptr;   // field scan buffer (global-memory slice vectors), or null
