@@ -88,8 +88,6 @@ struct FineArgs {
   Status* status;
   long long* prof;       // [6] optional phase profile (pk_debug_profile), or null
   long long* rowcnt;     // [2B] optional per-slice row counters (pk_count_rows), or null
-  long long stagger;     // software groups: group q starts its steps (q % stagger_mod) * stagger
-  int stagger_mod;       // cycles late (experiment knob PK_SG_STAGGER / PK_SG_STAGGER_MOD)
 };
 
 struct LiftArgs {

@@ -39,6 +39,12 @@ __device__ __forceinline__ double qdiv(double x, double d, double rd) {
 #endif
 }
 
+// profiling counters: a fire-and-forget reduction (no load round trip on
+// the profiled thread's timeline)
+__device__ __forceinline__ void pk_red_add(long long* p, long long v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
 // numpy pairwise-summation plan for an n-term reduction (numpy's
 // pairwise_sum: <8 sequential, <=128 eight accumulators, else split at
 // n/2 rounded down to a multiple of 8).  Leaves in order, internal nodes
@@ -339,18 +345,30 @@ __device__ __forceinline__ void pw_perfect(F x, const PwPlan& P, double* scr, do
 // violation (uniform over the block).
 template <class FA>
 __device__ bool field_exact_onchip(FA absrho, double* x, int nx, double dx, double rtol,
-                                   const PwPlan& P, double* red, double& mean) {
+                                   const PwPlan& P, double* red, double& mean,
+                                   long long* dbg = nullptr) {
+  long long c0 = dbg ? clock64() : 0;
+  auto tick = [&](int k) {  // optional stage profile (thread 0)
+    if (dbg && threadIdx.x == 0) {
+      const long long c1 = clock64();
+      pk_red_add(dbg + k, c1 - c0);
+      c0 = c1;
+    }
+  };
   double r[2];
   if (P.perfect)
     pw_perfect<2>([&](int s, int i) { return s ? absrho(i) : x[i]; }, P, red, r);
   else
     block_pairwise2([&](int i) { return x[i]; }, absrho, P, red, r[0], r[1]);
+  tick(0);
   if (fabs(r[0]) > rtol * fmax(r[1] * dx, 2.2250738585072014e-308)) return false;
   const double corr = r[0] / (double)nx;
   for (int i = threadIdx.x; i < nx; i += blockDim.x) x[i] = x[i] - corr;
   __syncthreads();
+  tick(1);
   smem_cumsum(x, x, nx);
   __syncthreads();
+  tick(2);
   if (P.perfect) {
     double mm[1];
     pw_perfect<1>([&](int, int i) { return x[i]; }, P, red, mm);
@@ -358,6 +376,7 @@ __device__ bool field_exact_onchip(FA absrho, double* x, int nx, double dx, doub
   } else {
     mean = block_pairwise([&](int i) { return x[i]; }, P, red) / (double)nx;
   }
+  tick(3);
   return true;
 }
 
@@ -396,12 +415,6 @@ __device__ void block_scan_fast(FS src, FD dst, int n, double* scratch) {
     dst(i, run);
   }
   __syncthreads();
-}
-
-// profiling counters: a fire-and-forget reduction (no load round trip on
-// the profiled thread's timeline)
-__device__ __forceinline__ void pk_red_add(long long* p, long long v) {
-  atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
 __device__ __forceinline__ int wrap(int i, int n) {

@@ -2607,11 +2607,6 @@ __global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs 
   // optional row counters (pk_count_rows): the slice owner's thread 0
   const bool rcnt = a.rowcnt && leader && threadIdx.x == 0;
   long long rc_rows = 0, rc_zero = 0;
-  if (a.stagger > 0) {  // experiment: desynchronise the software groups' steps
-    const long long d = (long long)((blockIdx.x / (unsigned)C) % (unsigned)a.stagger_mod) * a.stagger;
-    const long long t0 = clock64();
-    while (clock64() - t0 < d) __nanosleep(256);
-  }
   for (int s = 0; s < nst_all; ++s) {
     const int ph = s < n0 ? 0 : 1;
     if constexpr (AD) {  // rows the slice phase listed for zeroing in this step's output
@@ -2990,12 +2985,6 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
     }
   }
   const bool sg = a.sg > 1;
-  {
-    static const long long stg = getenv("PK_SG_STAGGER") ? atoll(getenv("PK_SG_STAGGER")) : 0;
-    static const int stm = getenv("PK_SG_STAGGER_MOD") ? atoi(getenv("PK_SG_STAGGER_MOD")) : 2;
-    a.stagger = sg ? stg : 0;
-    a.stagger_mod = stm > 0 ? stm : 2;
-  }
   if (dbg_packing)
     fprintf(stderr, "pk packing: B %d, %s of %d CTAs x %d slices\n", a.B,
             a.sg > 1 ? "software group" : "cluster", C, a.kps);

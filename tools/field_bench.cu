@@ -28,6 +28,8 @@ __device__ bool field_passes(const double* rho, double* x, int nx, double dx, co
   return true;
 }
 
+__device__ long long g_st[4];
+
 __global__ void bench(const PwPlan* gP, double* out, long long* t, int nx, int reps) {
   extern __shared__ double sm[];
   __shared__ PwPlan P;
@@ -48,7 +50,7 @@ __global__ void bench(const PwPlan* gP, double* out, long long* t, int nx, int r
       double mean = 0.0;
       bool ok;
       if (v == 0) ok = field_passes(rho, x, nx, dx, P, red, mean);
-      else ok = field_exact_onchip([&](int i) { return fabs(rho[i]); }, x, nx, dx, 1e300, P, red, mean);
+      else ok = field_exact_onchip([&](int i) { return fabs(rho[i]); }, x, nx, dx, 1e300, P, red, mean, g_st);
       __syncthreads();
       tot += clock64() - c0;
       acc += ok ? mean + x[nx - 1] : 0.0;
@@ -103,6 +105,10 @@ int main() {
       bench<<<1, nt, smem>>>(dP, out, t, nx, 20);
       long long h[2];
       cudaError_t e = cudaMemcpy(h, t, sizeof(h), cudaMemcpyDeviceToHost);
+      long long st[4], z[4] = {0, 0, 0, 0};
+      cudaMemcpyFromSymbol(st, g_st, sizeof(st));
+      cudaMemcpyToSymbol(g_st, z, sizeof(z));
+      printf("   onchip stages per call: sums %lld corr %lld chain %lld mean %lld\n", st[0] / 20, st[1] / 20, st[2] / 20, st[3] / 20);
       printf("nx %5d NT %3d: passes %7lld  onchip %7lld cycles (%s)\n", nx, nt, h[0], h[1],
              cudaGetErrorString(e));
     }
