@@ -216,6 +216,10 @@ __device__ __forceinline__ double stencil_at(const double* v, int i, int nx, con
 // stencil_at on a register window w[o] = v[i + o - 3] (same terms, same order).
 // With the reference's table (m.stc_std) the zero terms it skips are known:
 // the offset-0 term of orders 1 and 3 -- no per-term test.
+// sqrt with +0 answered inline: the device sqrt takes a slow subroutine for
+// zero operands, and fluid interfaces have <g^2> = 0 (sqrt(+0) = +0: same bits)
+__device__ __forceinline__ double sqrt0(double x) { return x == 0.0 ? x : sqrt(x); }
+
 __device__ __forceinline__ double stencil_reg(const double (&w)[7], const MeshDev& m, int p) {
   double acc = 0.0;
   if (m.stc_std) {
@@ -689,6 +693,389 @@ __device__ __forceinline__ Par leader_par(const Smem& sm) {
   return P;
 }
 
+// Kinetic-row list segment (contiguous cells) for the one-scan klist/kstream:
+// cnt kinetic cells, the first/last of them, and the stream rows its entries
+// after the first add (each entry q adds min(3, i_q - i_{q-1}) rows, the
+// first entry of the whole list 3).  Associative (segment A then B).
+struct KSeg {
+  int cnt, first, last, inner;
+};
+
+__device__ __forceinline__ KSeg kseg_comb(const KSeg& a, const KSeg& b) {
+  KSeg r;
+  r.cnt = a.cnt + b.cnt;
+  r.first = a.cnt ? a.first : b.first;
+  r.last = b.cnt ? b.last : a.last;
+  r.inner = a.inner + b.inner + ((a.cnt && b.cnt) ? min(3, b.first - a.last) : 0);
+  return r;
+}
+
+__device__ __forceinline__ KSeg kseg_shfl_up(const KSeg& x, int o) {
+  KSeg r;
+  r.cnt = __shfl_up_sync(FULL, x.cnt, o);
+  r.first = __shfl_up_sync(FULL, x.first, o);
+  r.last = __shfl_up_sync(FULL, x.last, o);
+  r.inner = __shfl_up_sync(FULL, x.inner, o);
+  return r;
+}
+
+// Block-wide exclusive scan of KSeg (thread order); returns the total.
+// `wt`: 4 * nwarp ints of shared memory.  One barrier.
+__device__ KSeg kseg_block_scan(const KSeg& mine, KSeg& excl, int* wt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const KSeg id = {0, 0, 0, 0};
+  KSeg inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const KSeg y = kseg_shfl_up(inc, o);
+    if (lane >= o) inc = kseg_comb(y, inc);
+  }
+  if (lane == 31) {
+    wt[4 * warp] = inc.cnt;
+    wt[4 * warp + 1] = inc.first;
+    wt[4 * warp + 2] = inc.last;
+    wt[4 * warp + 3] = inc.inner;
+  }
+  KSeg e = kseg_shfl_up(inc, 1);
+  if (lane == 0) e = id;
+  __syncthreads();
+  KSeg wp = id, tot = id;
+  for (int w = 0; w < nwarp; ++w) {
+    const KSeg t = {wt[4 * w], wt[4 * w + 1], wt[4 * w + 2], wt[4 * w + 3]};
+    if (w < warp) wp = kseg_comb(wp, t);
+    tot = kseg_comb(tot, t);
+  }
+  excl = kseg_comb(wp, e);
+  return tot;
+}
+
+// prepare_step's hybrid slice phase for ONE CTA (the leader alone; vectors in
+// shared or global memory): the same values as the pass-by-pass form below
+// with fewer passes and barriers -- J, (E - E_prev)/dt and J_c in one pass
+// (J_{i-1} recomputed: same operands, same bits), the masked moment b_m folded
+// into the dco pass (b_m(i +- 1) recomputed from the OLD kinetic-interface
+// flags, so the new labels are stored only after the scan's barrier), and the
+// kinetic-row list with its stream positions from ONE block scan of KSeg
+// segments.  The field's pending zero-mean shift (v.Emean) is applied where E
+// is read and stored in the dco pass, where no other thread reads E.
+template <int T>
+__device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Smem& sm, double dt,
+                                 int moment_all, double* gin, uint8_t* nzin, uint8_t* nzout,
+                                 int step, long long* dbg) {
+  long long c0 = dbg ? clock64() : 0;
+  auto tick = [&](int k) {
+    if (dbg && threadIdx.x == 0) {
+      const long long c1 = clock64();
+      pk_red_add(dbg + k, c1 - c0);
+      c0 = c1;
+    }
+  };
+  const MeshDev& m = a.m;
+  const int nx = m.nx, nv = m.nv;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  int* sflags = sm.misc;  // [0] any flip, [40]/[41] list sizes, [8..) scan scratch
+  const double Em = v.Emean;
+  const double* __restrict__ rho_ = v.rho;
+  double* __restrict__ E_ = v.E;
+  const double* __restrict__ Ep_ = v.Eprev;
+  auto Ef = [&](int i) { return E_[i] - Em; };  // x - 0.0 == x when nothing is pending
+  if (tid == 0) {
+    sflags[0] = 0;
+    sflags[40] = 0;
+    sflags[41] = 0;
+  }
+  // P1: J (fluid.py:48-52), (E - E_prev)/dt, J_c = (J_{i-1} + J_i)/2
+  {
+    const double rdt = 1.0 / dt;
+    double* __restrict__ J_ = v.J;
+    double* __restrict__ gJ_ = v.gJ;
+    double* __restrict__ tA_ = v.tA;
+    double* __restrict__ tB_ = v.tB;
+    constexpr int U = 2;
+    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+      double rm[U], r0[U], r1[U], em[U], e0[U], ep[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nx - 1);
+        const int ip = wrap(i - 1, nx);
+        rm[u] = rho_[ip];
+        r0[u] = rho_[i];
+        r1[u] = rho_[wrap(i + 1, nx)];
+        em[u] = Ef(ip);
+        e0[u] = Ef(i);
+        ep[u] = Ep_[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nt;
+        if (i < nx) {
+          const double J = flux_J(r0[u], r1[u], e0[u], m.dx, m.rdx);
+          const double Jm = flux_J(rm[u], r0[u], em[u], m.dx, m.rdx);
+          J_[i] = J;
+          gJ_[i] = J;
+          tA_[i] = qdiv(e0[u] - ep[u], dt, rdt);
+          tB_[i] = 0.5 * (Jm + J);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  tick(0);
+  // P2: remainder indicator (adaptation.py:120-152), perturbation norm
+  // (155-159), labels (161-181)
+  {
+    const double three_rb = 3.0 * v.rb;
+    const double* __restrict__ tA_ = v.tA;
+    const double* __restrict__ tB_ = v.tB;
+    const double* __restrict__ sq_ = v.sq;
+    const uint8_t* __restrict__ ki_ = v.ki;
+    double* __restrict__ tC_ = v.tC;
+    double* __restrict__ tD_ = v.tD;
+    uint8_t* __restrict__ kcn_ = v.kcn;
+    const double* __restrict__ rsc = a.rscale ? a.rscale + (size_t)v.b * nx : nullptr;
+    constexpr int U = 2;
+    for (int i0 = tid; i0 < nx; i0 += U * nt) {
+      double wB[U][7], wR[U][7], a0[U], a1[U], e0[U], e1[U], s0[U], s1[U], rs[U];
+      int k0[U], k1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i0 + u * nt, nx - 1);
+        const int ip = wrap(i - 1, nx);
+#pragma unroll
+        for (int o = 0; o < 7; ++o) {
+          const int j = wrap(i + o - 3, nx);
+          wB[u][o] = tB_[j];
+          wR[u][o] = rho_[j];
+        }
+        a0[u] = tA_[ip];
+        a1[u] = tA_[i];
+        e0[u] = Ef(ip);
+        e1[u] = Ef(i);
+        s0[u] = sq_[ip];
+        s1[u] = sq_[i];
+        k0[u] = ki_[ip];
+        k1[u] = ki_[i];
+        rs[u] = rsc ? rsc[i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nt;
+        if (i < nx) {
+          const double dtEc = 0.5 * (a0[u] + a1[u]);
+          const double Ec = 0.5 * (e0[u] + e1[u]);
+          const double d1J = stencil_reg(wB[u], m, 1);
+          const double d2J = stencil_reg(wB[u], m, 2);
+          const double d3J = stencil_reg(wB[u], m, 3);
+          const double d1r = stencil_reg(wR[u], m, 1);
+          const double rho = wR[u][3];
+          const double Jc = wB[u][3];
+          const double R =
+              -d3J + Ec * d2J + (2.0 * rho - three_rb) * d1J + 2.0 * Jc * d1r - d1r * dtEc;
+          tC_[i] = R;    // unscaled R (lift, higher_order)
+          tD_[i] = d1J;  // D1(J_c) (lift drift)
+          const double Rs = rsc ? rs[u] * R : R;
+          const double sqp = (moment_all || k0[u]) ? s0[u] : 0.0;
+          const double sqi = (moment_all || k1[u]) ? s1[u] : 0.0;
+          const double gn = sqrt0(0.5 * (sqp + sqi));
+          const bool fR = fabs(Rs) < a.delta0;
+          const bool fg = gn < a.eta0;
+          const bool fluid = a.combine_and ? (fR && fg) : (fR || fg);
+          kcn_[i] = fluid ? 0 : 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  tick(1);
+  // P3: kinetic interfaces and F -> K flips, listed (klist is free until the
+  // row list below)
+  int anyflip = 0;
+  {
+    const uint8_t* __restrict__ kcn_ = v.kcn;
+    const uint8_t* __restrict__ ki_ = v.ki;
+    uint8_t* __restrict__ kin_ = v.kin;
+    uint8_t* __restrict__ flip_ = v.flip;
+    constexpr int U = 4;
+    for (int i00 = 0; i00 < nx; i00 += U * nt) {  // uniform trip count (ballots inside)
+      int c0v[U], c1v[U], k[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i00 + u * nt + tid, nx - 1);
+        c0v[u] = kcn_[i];
+        c1v[u] = kcn_[wrap(i + 1, nx)];
+        k[u] = ki_[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i00 + u * nt + tid;
+        uint8_t f = 0;
+        if (i < nx) {
+          const uint8_t kin = (uint8_t)(c0v[u] | c1v[u]);
+          kin_[i] = kin;
+          f = (kin && !k[u]) ? 1 : 0;
+          flip_[i] = f;
+        }
+        anyflip |= f;
+        list_append(f != 0, i, v.klist, &sflags[40]);
+      }
+    }
+  }
+  if (anyflip) atomicOr(&sflags[0], 1);
+  __syncthreads();
+  tick(2);
+  const int nflip = sflags[40];
+  if (dbg && tid == 0) pk_red_add(dbg + 10, nflip);
+  if (sflags[0]) {
+    if (a.reinit == 0) {
+      if (a.lift_order != 1 && a.lift_order != 2) {
+        if (tid == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
+        return false;
+      }
+      if (a.lift_order >= 2 && a.time_elim != 0 && a.time_elim != 1) {
+        if (tid == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
+        return false;
+      }
+      // lift scalars at the flipped interfaces (lifting.py:63-88); dE_dt = (E - E_prev)/dt
+      for (int q = tid; q < nflip; q += nt) {
+        const int i = v.klist[q];
+        const int in_ = wrap(i + 1, nx);
+        const double dJ = 0.5 * (v.tD[i] + v.tD[in_]);
+        v.tE[i] = dJ - Ef(i) * v.J[i];           // drift
+        v.tA[i] = 0.5 * (v.tC[i] + v.tC[in_]);   // R_if
+      }
+      __syncthreads();
+      for (int q = warp; q < nflip; q += nt >> 5) {
+        const int i = v.klist[q];
+        LiftRow L;
+        const size_t o = (size_t)v.b * nx + i;
+        L.negJ = a.neg_eps[o] * v.J[i];
+        L.e2 = a.eps2[o];
+        L.drift = v.tE[i];
+        L.Rif = v.tA[i];
+        double bx, bsq;
+        if constexpr (T < 0) {
+          double* row = gin + (size_t)i * nv;
+          double* scr = sm.wrow + warp * BIG_SCR;
+          big_row_lift(row, L, a.lift_order, a.time_elim == 1, 1, m, scr, lane);
+          big_row_moments(row, m, scr, false, bx, bsq);
+        } else {
+          double g[Layout<T>::S];
+          row_lift<T>(g, L, a.lift_order, a.time_elim == 1, 1, sm, m, sm.wrow + warp * nv, lane);
+          row_store<T>(g, gin + (size_t)i * nv, lane, nv);
+          row_moments<T>(g, sm, m, sm.wrow + warp * nv, lane, bx, bsq);
+        }
+        if (lane == 0) v.blift[i] = bx;
+      }
+    } else if (a.reinit == 1) {
+      for (int q = warp; q < nflip; q += nt >> 5) {
+        const int i = v.klist[q];
+        row_zero_store<T>(gin + (size_t)i * nv, lane, nv);
+        if (lane == 0) v.blift[i] = 0.0;
+      }
+    } else {
+      if (tid == 0) set_status(a.status, PK_ERR_BAD_REINIT, v.b, step);
+      return false;
+    }
+    __syncthreads();
+  }
+  tick(3);
+  // P4: masked projection moment b_m (hybrid.py:103-105) at i-1, i+1 from the
+  // post-flip rows and the OLD interface flags, dco (kinetic.py:190-191),
+  // E-upwind factors (177-178), the zero list (hybrid.py:166), E stored
+  {
+    const uint8_t* __restrict__ ki_ = v.ki;
+    const uint8_t* __restrict__ kin_ = v.kin;
+    const uint8_t* __restrict__ flip_ = v.flip;
+    const double* __restrict__ blift_ = v.blift;
+    const double* __restrict__ fl_ = v.fl;
+    double* __restrict__ dco_ = v.dco;
+    double* __restrict__ vco_ = v.vco;
+    int8_t* __restrict__ vsg_ = v.vsg;
+    uint8_t* __restrict__ nzo = nzout;
+    auto bm = [&](int j) {
+      const bool valid = moment_all || ki_[j];
+      return kin_[j] ? (flip_[j] ? blift_[j] : (valid ? fl_[j] : 0.0)) : 0.0;
+    };
+    const bool pend = v.Epend;
+    constexpr int U = 2;
+    for (int i00 = 0; i00 < nx; i00 += U * nt) {  // uniform trip count (ballots inside)
+      double b1[U], b0[U], e[U];
+      int kn[U], nz[U], fp[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = min(i00 + u * nt + tid, nx - 1);
+        b1[u] = bm(wrap(i + 1, nx));
+        b0[u] = bm(wrap(i - 1, nx));
+        e[u] = Ef(i);
+        kn[u] = kin_[i];
+        nz[u] = nzo[i];
+        fp[u] = flip_[i];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i00 + u * nt + tid;
+        bool z = false;
+        if (i < nx) {
+          dco_[i] = qdiv(b1[u] - b0[u], m.two_dx, m.rtwo_dx);
+          vsg_[i] = e[u] > 0.0 ? 1 : (e[u] < 0.0 ? -1 : 0);
+          vco_[i] = qdiv(e[u], m.dvx, m.rdvx);
+          if (pend) E_[i] = e[u];
+          if (!moment_all && fp[u]) nzin[i] = 1;
+          z = !kn[u] && nz[u];
+          if (z) nzo[i] = 0;
+        }
+        list_append(z, i, v.zlist, &sflags[41]);
+      }
+    }
+  }
+  tick(5);
+  // P5: the order-preserving kinetic-row list and its row-stream positions
+  // (one KSeg scan over contiguous chunks); the new labels stored
+  {
+    const uint8_t* __restrict__ kin_ = v.kin;
+    const int per = (nx + nt - 1) / nt;
+    const int lo = min(nx, tid * per), hi = min(nx, lo + per);
+    KSeg mine = {0, 0, 0, 0};
+    for (int i = lo; i < hi; ++i)
+      if (kin_[i]) {
+        if (mine.cnt) mine.inner += min(3, i - mine.last);
+        else mine.first = i;
+        mine.last = i;
+        ++mine.cnt;
+      }
+    KSeg ex;
+    const KSeg tot = kseg_block_scan(mine, ex, sflags + 8);  // (barrier: P4 is done)
+    int q = ex.cnt, prev = ex.last;
+    int pos = ex.cnt ? 3 + ex.inner : 0;  // stream rows of the entries before this chunk
+    for (int i = lo; i < hi; ++i) {
+      v.kc[i] = v.kcn[i];
+      const uint8_t kn = kin_[i];
+      v.ki[i] = kn;
+      if (kn) {
+        const int nn = q == 0 ? 3 : min(3, i - prev);
+        pos += nn;
+        v.klist[q] = i;
+        v.kpos[q] = pos;
+        for (int t = 0; t < nn; ++t) v.kstream[pos - nn + t] = i + 2 - nn + t;
+        prev = i;
+        ++q;
+      }
+    }
+    if (tid == 0) {
+      *v.nk = tot.cnt;
+      *v.nzl = sflags[41];
+      if (dbg) {
+        pk_red_add(dbg + 11, sflags[41]);
+        pk_red_add(dbg + 12, tot.cnt);
+      }
+    }
+  }
+  __syncthreads();
+  tick(7);
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // Slice phase: prepare step `s` (labels, flips, projection coefficients, row
 // list) from rho, E (start of step s), Eprev and the moments fl/sq of the
@@ -733,6 +1120,8 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     return true;
   }
 
+  if (!P.dist && !a.pass_prepare)
+    return prepare_step_cta<T>(a, v, sm, dt, moment_all, gin, nzin, nzout, step, dbg);
   // The element loops below run over global memory when the slice vectors do
   // not fit on chip (large nx): every operand of U iterations is loaded
   // unconditionally first (restrict views, no load behind a branch), so the
@@ -851,7 +1240,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
           // perturbation indicator (adaptation.py:155-159) on the incoming g
           const double sqp = (moment_all || k0[u]) ? s0[u] : 0.0;
           const double sqi = (moment_all || k1[u]) ? s1[u] : 0.0;
-          const double gn = sqrt(0.5 * (sqp + sqi));
+          const double gn = sqrt0(0.5 * (sqp + sqi));
           const bool fR = fabs(Rs) < a.delta0;
           const bool fg = gn < a.eta0;
           const bool fluid = a.combine_and ? (fR && fg) : (fR || fg);
@@ -2985,6 +3374,8 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
     }
   }
   const bool sg = a.sg > 1;
+  static const bool pass_prepare = getenv("PK_PASS_PREPARE") != nullptr;
+  a.pass_prepare = pass_prepare ? 1 : 0;
   if (dbg_packing)
     fprintf(stderr, "pk packing: B %d, %s of %d CTAs x %d slices\n", a.B,
             a.sg > 1 ? "software group" : "cluster", C, a.kps);
@@ -3106,7 +3497,7 @@ __global__ void __launch_bounds__(256) gnorm_kernel(const IndArgs a) {
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nx; i += blockDim.x)
-    a.gnorm[(size_t)b * nx + i] = sqrt(0.5 * (sq[wrap(i - 1, nx)] + sq[i]));
+    a.gnorm[(size_t)b * nx + i] = sqrt0(0.5 * (sq[wrap(i - 1, nx)] + sq[i]));
 }
 
 // labels (update_labels, DomainLabels.from_cells; adaptation.py:100-105,162-181)
