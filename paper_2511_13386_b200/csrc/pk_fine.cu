@@ -2749,7 +2749,9 @@ __device__ __forceinline__ void group_barrier(unsigned* cnt, int C, unsigned& n)
 // AD: adaptation on (hybrid) or off (all-kinetic, compiled without the
 // labels / lifts / row lists of the hybrid slice phase)
 template <int T, int S, int G, int NT, bool AD>
-__global__ void __launch_bounds__(NT, T < 0 ? 1 : 2) fine_kernel(const FineArgs a) {
+// (the G8 layouts with 8 warps run one CTA per SM: the full register file)
+__global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128)) ? 1 : 2)
+    fine_kernel(const FineArgs a) {
   // ring row stride (doubles); G > 0: per-warp G8 rings, G < 0: CTA-wide
   // producer/consumer ring of the GS layout with SEG = -G
   constexpr int RSN = G > 0 ? 16 * G + 8 : (G < 0 ? 64 * (-G) + 8 : 32 * (T > 0 ? T : 1));
@@ -3296,6 +3298,33 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   auto kern = fine_kernel<T, S, G, NT, AD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if constexpr (G > 0 && NT > 128) {
+    // the 8-warp G8 layout only when every cluster of the grid is resident
+    // at one CTA per SM; else the caller falls back to 4 warps
+    if ((size_t)a.B * C > (size_t)num_sms) return cudaErrorNotSupported;
+    if (C > 1) {
+      if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                       cudaSuccess)
+        return cudaErrorNotSupported;
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3(C);
+      qc.blockDim = dim3(NT);
+      qc.dynamicSmemBytes = smem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = C;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &qc) != cudaSuccess) {
+        cudaGetLastError();
+        return cudaErrorNotSupported;
+      }
+      if (n < a.B) return cudaErrorNotSupported;
+    }
+  }
   static const bool dbg_packing = getenv("PK_DEBUG_PACKING") != nullptr;
   const bool autok = a.kps == 0;
   a.kps = 1;
@@ -3558,12 +3587,32 @@ cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   }
   if ((a.m.nv == 64 || a.m.nv == 128) && !a.m.mirror)  // G8 needs the mirrored grid
     return launch_T<0, 1, 0, 256>(a, C, st);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // a grid of at most one CTA per SM (few, latency-bound slices: parareal
+  // windows): 8 warps per CTA at the full register file -- half the rows per
+  // warp and half the cells per thread in the slice phase
+  // (launch_TA may still halve C; it refuses the wide layout with
+  // cudaErrorNotSupported unless every cluster is resident)
+  static const bool no_wide = getenv("PK_NO_WIDE") != nullptr;
+  const bool wide = !no_wide && (long long)a.B * (C > 1 ? C / 2 : 1) <= nsm;
+  cudaError_t e = cudaErrorNotSupported;
   switch (a.m.nv) {
     // producer/consumer GS pipeline: 7 consumer warps + 1 producer warp
-    case 64: return launch_T<2, 16, 4, 128>(a, C, st);   // G8 per-warp rings, 4 warps
-    case 128: return launch_T<4, 14, 8, 128>(a, C, st);  // G8 per-warp rings, 4 warps
-      // (8 warps at <= 128 registers: no spills, but the micro loop loses its
-      // ILP and the step takes 1.6x longer)
+    case 64:  // G8 per-warp rings, 4 warps (8 at one CTA per SM)
+      if (wide) e = launch_T<2, 16, 4, 256>(a, C, st);
+      if (e == cudaErrorNotSupported) e = launch_T<2, 16, 4, 128>(a, C, st);
+      return e;
+    case 128:
+      if (wide) e = launch_T<4, 14, 8, 256>(a, C, st);
+      if (e == cudaErrorNotSupported) e = launch_T<4, 14, 8, 128>(a, C, st);
+      return e;
+      // (8 warps at two CTAs per SM, <= 128 registers: no spills, but the micro
+      // loop loses its ILP and the step takes 1.6x longer)
     case 256: return launch_T<8, 20, -4, 256>(a, C, st);
     case 512: return launch_T<16, 3, 0, 256>(a, C, st);
     default:
