@@ -297,27 +297,51 @@ __device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int 
 // meet in `scr` (NS nleaf / 4 doubles) behind ONE barrier and every warp
 // finishes the tree itself; the caller keeps a barrier between this call's
 // reads of scr and the next writes to it.
+// One full numpy leaf of 128 terms at x(off ..) per 8-lane group: eight
+// interleaved accumulators (16 operands loaded back to back), the 8-way
+// butterfly.  group_leaf's n == 128 case with the length known at compile time.
+template <class F>
+__device__ __forceinline__ double leaf128(F x, int off) {
+  const int k = threadIdx.x & 7;
+  double t[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) t[j] = x(off + 8 * j + k);
+  double r = t[0];
+#pragma unroll
+  for (int j = 1; j < 16; ++j) r = r + t[j];
+  r = r + __shfl_xor_sync(FULL, r, 1);
+  r = r + __shfl_xor_sync(FULL, r, 2);
+  r = r + __shfl_xor_sync(FULL, r, 4);
+  return r;
+}
+
 template <int NS, class F>
 __device__ __forceinline__ void pw_perfect(F x, const PwPlan& P, double* scr, double (&res)[NS]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int nl = P.nleaf, ntask = NS * nl;
+  const int lg = __ffs(nl) - 1;                // nl = 2^lg
+  const bool full = P.n == (nl << 7);          // every leaf 128 terms: leaf l at 128 l
+  auto leaf = [&](int s, int l, bool act) {
+    return full ? leaf128([&](int i) { return x(s, i); }, l << 7)
+                : group_leaf([&](int i) { return x(s, i); }, act ? P.leaf_off[l] : 0,
+                             act ? P.leaf_len[l] : 0, act);
+  };
   if (ntask <= 4) {
     const int t = lane >> 3;
     const bool act = t < ntask;
-    const int s = act ? t / nl : 0, l = act ? t - s * nl : 0;
-    double v = group_leaf([&](int i) { return x(s, i); }, act ? P.leaf_off[l] : 0,
-                          act ? P.leaf_len[l] : 0, act);
+    const int s = act ? t >> lg : 0, l = act ? t - (s << lg) : 0;
+    double v = leaf(s, act ? l : 0, act);
     if (nl >= 2) v = v + __shfl_xor_sync(FULL, v, 8);
     if (nl >= 4) v = v + __shfl_xor_sync(FULL, v, 16);
 #pragma unroll
-    for (int q = 0; q < NS; ++q) res[q] = __shfl_sync(FULL, v, 8 * nl * q);
+    for (int q = 0; q < NS; ++q) res[q] = __shfl_sync(FULL, v, (8 << lg) * q);
     return;
   }
   // nl >= 4 here (a power of two): aligned groups of four leaves share a sum
   for (int t0 = 4 * warp; t0 < ntask; t0 += 4 * nwarp) {
     const int t = t0 + (lane >> 3);
-    const int s = t / nl, l = t - s * nl;
-    double v = group_leaf([&](int i) { return x(s, i); }, P.leaf_off[l], P.leaf_len[l], true);
+    const int s = t >> lg, l = t - (s << lg);
+    double v = leaf(s, l, true);
     v = v + __shfl_xor_sync(FULL, v, 8);
     v = v + __shfl_xor_sync(FULL, v, 16);
     if (lane == 0) scr[t0 >> 2] = v;
@@ -356,8 +380,9 @@ __device__ bool field_exact_onchip(FA absrho, double* x, int nx, double dx, doub
     }
   };
   double r[2];
+  const uint32_t xs = (uint32_t)__cvta_generic_to_shared(x);  // x is in shared memory
   if (P.perfect)
-    pw_perfect<2>([&](int s, int i) { return s ? absrho(i) : x[i]; }, P, red, r);
+    pw_perfect<2>([&](int s, int i) { return s ? absrho(i) : lds64(xs + 8 * i); }, P, red, r);
   else
     block_pairwise2([&](int i) { return x[i]; }, absrho, P, red, r[0], r[1]);
   tick(0);
@@ -371,7 +396,7 @@ __device__ bool field_exact_onchip(FA absrho, double* x, int nx, double dx, doub
   tick(2);
   if (P.perfect) {
     double mm[1];
-    pw_perfect<1>([&](int, int i) { return x[i]; }, P, red, mm);
+    pw_perfect<1>([&](int, int i) { return lds64(xs + 8 * i); }, P, red, mm);
     mean = mm[0] / (double)nx;
   } else {
     mean = block_pairwise([&](int i) { return x[i]; }, P, red) / (double)nx;

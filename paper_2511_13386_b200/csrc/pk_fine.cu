@@ -552,8 +552,9 @@ __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, doub
     }
     PK_TICK(0)
     double mean;
-    if (!field_exact_onchip([&](int i) { return fabs(rho[i]); }, E_out, nx, m.dx, rtol, *sm.plan,
-                            sm.red, mean))
+    const uint32_t rs = (uint32_t)__cvta_generic_to_shared(rho);  // on chip: shared memory
+    if (!field_exact_onchip([&](int i) { return fabs(lds64(rs + 8 * i)); }, E_out, nx, m.dx, rtol,
+                            *sm.plan, sm.red, mean))
       return false;
     PK_TICK(3)
     if (mean_out) {  // the caller applies E - mean where it next reads E
