@@ -15,6 +15,7 @@ namespace pk {
 // solvability violation, else E holds cumsum(src - defect/nx) and `mean` its
 // mean, so the field is E[i] - mean (poisson.py:41-54; the subtraction is
 // applied where E is read, with the same rounding).  E doubles as src.
+// Exact, up to 256 threads: field_exact_onchip.
 template <int NT>
 __device__ static bool chain_field(const MeshDev& m, const double* rho, double rb, double* E,
                                    double rtol, int exact_scan, const PwPlan& plan, double* red,
@@ -22,6 +23,13 @@ __device__ static bool chain_field(const MeshDev& m, const double* rho, double r
   const int nx = m.nx;
   for (int i = threadIdx.x; i < nx; i += NT) E[i] = (rho[i] - rb) * m.dx;
   __syncthreads();
+  if constexpr (NT <= 256) {  // (the 512-thread instantiations spill with it)
+    if (exact_scan) {
+      const uint32_t rs = (uint32_t)__cvta_generic_to_shared(rho);
+      return field_exact_onchip([&](int i) { return fabs(lds64(rs + 8 * i)); }, E, nx, m.dx,
+                                rtol, plan, red, mean);
+    }
+  }
   double defect, abssum;
   block_pairwise2([&](int i) { return E[i]; }, [&](int i) { return fabs(rho[i]); }, plan, red,
                   defect, abssum);
