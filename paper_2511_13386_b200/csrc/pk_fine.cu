@@ -3328,6 +3328,45 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   }
   static const bool dbg_packing = getenv("PK_DEBUG_PACKING") != nullptr;
   const bool autok = a.kps == 0;
+  // Few large slices (e.g. cfg4's 8 windows per GPU of 8192 cells: 64 CTAs on
+  // 148 SMs): grow the 8-CTA clusters up to 16 CTAs while every cluster of
+  // the grid stays resident (GPC packing: 12 x 8 does not fit, 10 x 8 does)
+  // and every warp keeps >= 8 rows -- the micro phase shrinks with the share.
+  static const bool no_grow = getenv("PK_NO_GROW") != nullptr;
+  if (!no_grow && autok && C == 8 && !a.bigc && T != 0 &&
+      (long long)a.m.nx >= 9LL * (NT / 32) * 8 && (size_t)a.B * 9 <= 2 * (size_t)num_sms) {
+    static size_t g_smem = 0;
+    static int g_max[17];
+    if (g_smem != smem) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      for (int cc = 9; cc <= 16; ++cc) {
+        cudaLaunchConfig_t qc = {};
+        qc.gridDim = dim3(cc);
+        qc.blockDim = dim3(NT);
+        qc.dynamicSmemBytes = smem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = cc;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &qc) != cudaSuccess) {
+          cudaGetLastError();
+          n = 0;
+        }
+        g_max[cc] = n;
+      }
+      g_smem = smem;
+    }
+    for (int cc = 16; cc > 8; --cc)
+      if (g_max[cc] >= a.B && (long long)a.m.nx >= (long long)cc * (NT / 32) * 8) {
+        C = cc;
+        break;
+      }
+  }
   a.kps = 1;
   a.sg = 0;
   if constexpr (!AD && G > 0) {
