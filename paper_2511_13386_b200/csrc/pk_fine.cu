@@ -750,9 +750,10 @@ __device__ KSeg kseg_block_scan(const KSeg& mine, KSeg& excl, int* wt) {
   return tot;
 }
 
-// prepare_step's hybrid slice phase for ONE CTA (the leader alone; vectors in
-// shared or global memory): the same values as the pass-by-pass form below
-// with fewer passes and barriers -- J, (E - E_prev)/dt and J_c in one pass
+// prepare_step's hybrid slice phase in five passes (the leader CTA alone, or
+// -- Par::dist -- every CTA of the cluster on global-memory vectors with
+// cluster barriers): the same values as the pass-by-pass form below with
+// fewer passes and barriers -- J, (E - E_prev)/dt and J_c in one pass
 // (J_{i-1} recomputed: same operands, same bits), the masked moment b_m folded
 // into the dco pass (b_m(i +- 1) recomputed from the OLD kinetic-interface
 // flags, so the new labels are stored only after the scan's barrier), and the
@@ -760,9 +761,9 @@ __device__ KSeg kseg_block_scan(const KSeg& mine, KSeg& excl, int* wt) {
 // segments.  The field's pending zero-mean shift (v.Emean) is applied where E
 // is read and stored in the dco pass, where no other thread reads E.
 template <int T>
-__device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Smem& sm, double dt,
-                                 int moment_all, double* gin, uint8_t* nzin, uint8_t* nzout,
-                                 int step, long long* dbg) {
+__device__ bool prepare_step_fused(const FineArgs& a, const SliceView& v, const Smem& sm,
+                                   double dt, int moment_all, double* gin, uint8_t* nzin,
+                                   uint8_t* nzout, int step, const Par& P, long long* dbg) {
   long long c0 = dbg ? clock64() : 0;
   auto tick = [&](int k) {
     if (dbg && threadIdx.x == 0) {
@@ -773,15 +774,15 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
   };
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  int* sflags = sm.misc;  // [0] any flip, [40]/[41] list sizes, [8..) scan scratch
+  const int tid = P.r0, nt = P.rs;  // this thread's first element, element stride
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int* sflags = P.flags;  // the leader's: [0] any flip, [40]/[41] list sizes
   const double Em = v.Emean;
   const double* __restrict__ rho_ = v.rho;
   double* __restrict__ E_ = v.E;
   const double* __restrict__ Ep_ = v.Eprev;
   auto Ef = [&](int i) { return E_[i] - Em; };  // x - 0.0 == x when nothing is pending
-  if (tid == 0) {
+  if (P.rank == 0 && threadIdx.x == 0) {
     sflags[0] = 0;
     sflags[40] = 0;
     sflags[41] = 0;
@@ -821,7 +822,7 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
       }
     }
   }
-  __syncthreads();
+  P.sync();
   tick(0);
   // P2: remainder indicator (adaptation.py:120-152), perturbation norm
   // (155-159), labels (161-181)
@@ -887,7 +888,7 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
       }
     }
   }
-  __syncthreads();
+  P.sync();
   tick(1);
   // P3: kinetic interfaces and F -> K flips, listed (klist is free until the
   // row list below)
@@ -923,18 +924,18 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
     }
   }
   if (anyflip) atomicOr(&sflags[0], 1);
-  __syncthreads();
+  P.sync();
   tick(2);
   const int nflip = sflags[40];
-  if (dbg && tid == 0) pk_red_add(dbg + 10, nflip);
+  if (dbg && threadIdx.x == 0) pk_red_add(dbg + 10, nflip);
   if (sflags[0]) {
     if (a.reinit == 0) {
       if (a.lift_order != 1 && a.lift_order != 2) {
-        if (tid == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
+        if (P.rank == 0 && threadIdx.x == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
         return false;
       }
       if (a.lift_order >= 2 && a.time_elim != 0 && a.time_elim != 1) {
-        if (tid == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
+        if (P.rank == 0 && threadIdx.x == 0) set_status(a.status, PK_ERR_BAD_LIFT, v.b, step);
         return false;
       }
       // lift scalars at the flipped interfaces (lifting.py:63-88); dE_dt = (E - E_prev)/dt
@@ -945,8 +946,8 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
         v.tE[i] = dJ - Ef(i) * v.J[i];           // drift
         v.tA[i] = 0.5 * (v.tC[i] + v.tC[in_]);   // R_if
       }
-      __syncthreads();
-      for (int q = warp; q < nflip; q += nt >> 5) {
+      P.sync();
+      for (int q = P.w0; q < nflip; q += P.ws) {
         const int i = v.klist[q];
         LiftRow L;
         const size_t o = (size_t)v.b * nx + i;
@@ -969,16 +970,16 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
         if (lane == 0) v.blift[i] = bx;
       }
     } else if (a.reinit == 1) {
-      for (int q = warp; q < nflip; q += nt >> 5) {
+      for (int q = P.w0; q < nflip; q += P.ws) {
         const int i = v.klist[q];
         row_zero_store<T>(gin + (size_t)i * nv, lane, nv);
         if (lane == 0) v.blift[i] = 0.0;
       }
     } else {
-      if (tid == 0) set_status(a.status, PK_ERR_BAD_REINIT, v.b, step);
+      if (P.rank == 0 && threadIdx.x == 0) set_status(a.status, PK_ERR_BAD_REINIT, v.b, step);
       return false;
     }
-    __syncthreads();
+    P.sync();
   }
   tick(3);
   // P4: masked projection moment b_m (hybrid.py:103-105) at i-1, i+1 from the
@@ -1046,7 +1047,25 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
         ++mine.cnt;
       }
     KSeg ex;
-    const KSeg tot = kseg_block_scan(mine, ex, sflags + 8);  // (barrier: P4 is done)
+    KSeg tot = kseg_block_scan(mine, ex, sm.misc + 8);  // (barrier: P4 is done here)
+    if (P.dist) {  // CTA totals meet in the leader's reduction scratch (free here)
+      int* ct = reinterpret_cast<int*>(cg::this_cluster().map_shared_rank(sm.red, 0)) + 576;
+      if (threadIdx.x == 0) {
+        ct[4 * P.rank] = tot.cnt;
+        ct[4 * P.rank + 1] = tot.first;
+        ct[4 * P.rank + 2] = tot.last;
+        ct[4 * P.rank + 3] = tot.inner;
+      }
+      P.sync();  // (also: every CTA's P4 is done)
+      KSeg pre = {0, 0, 0, 0}, all = {0, 0, 0, 0};
+      for (int r = 0; r < P.C; ++r) {
+        const KSeg t = {ct[4 * r], ct[4 * r + 1], ct[4 * r + 2], ct[4 * r + 3]};
+        if (r < P.rank) pre = kseg_comb(pre, t);
+        all = kseg_comb(all, t);
+      }
+      ex = kseg_comb(pre, ex);
+      tot = all;
+    }
     int q = ex.cnt, prev = ex.last;
     int pos = ex.cnt ? 3 + ex.inner : 0;  // stream rows of the entries before this chunk
     for (int i = lo; i < hi; ++i) {
@@ -1063,7 +1082,7 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
         ++q;
       }
     }
-    if (tid == 0) {
+    if (P.rank == 0 && threadIdx.x == 0) {
       *v.nk = tot.cnt;
       *v.nzl = sflags[41];
       if (dbg) {
@@ -1072,7 +1091,7 @@ __device__ bool prepare_step_cta(const FineArgs& a, const SliceView& v, const Sm
       }
     }
   }
-  __syncthreads();
+  P.sync();
   tick(7);
   return true;
 }
@@ -1121,8 +1140,8 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
     return true;
   }
 
-  if (!P.dist && !a.pass_prepare)
-    return prepare_step_cta<T>(a, v, sm, dt, moment_all, gin, nzin, nzout, step, dbg);
+  if (!a.pass_prepare)
+    return prepare_step_fused<T>(a, v, sm, dt, moment_all, gin, nzin, nzout, step, P, dbg);
   // The element loops below run over global memory when the slice vectors do
   // not fit on chip (large nx): every operand of U iterations is loaded
   // unconditionally first (restrict views, no load behind a branch), so the
