@@ -113,6 +113,26 @@ def per_value(values: np.ndarray, fn) -> np.ndarray:
 
 
 _COEF_ROWS: dict = {}   # (mesh, eps, dt) -> coefficient rows (insertion-ordered LRU)
+_EPS_ROWS: dict = {}    # (eps, nx, kind) -> (eps, row): -eps_i, eps_i**2, eps_c**2
+
+
+def _eps_row(eps, nx: int, kind: str) -> np.ndarray:
+    """-eps_i, eps_i**2 per interface or eps_c**2 per cell as Python floats per
+    distinct value (per_value), memoised per eps object: a parareal run passes
+    the same profile for every window."""
+    key = (id(eps) if hasattr(eps, "iface") else float(eps), nx, kind)
+    hit = _EPS_ROWS.get(key)
+    if hit is None or (hasattr(eps, "iface") and hit[0] is not eps):
+        if kind == "neg":
+            row = per_value(eps_rows(eps, nx), lambda v: -v)
+        elif kind == "sq":
+            row = per_value(eps_rows(eps, nx), lambda v: v**2)
+        else:
+            row = per_value(eps_cells(eps, nx), lambda v: v**2)
+        hit = _EPS_ROWS[key] = (eps, row)
+        while len(_EPS_ROWS) > 64:
+            _EPS_ROWS.pop(next(iter(_EPS_ROWS)))
+    return hit[1]
 
 
 def _coef_rows(mesh: PhaseMesh, eps, dt: float):
@@ -357,13 +377,13 @@ class Device:
         hyb.time_elim = {"leading": 0, "higher_order": 1}.get(knobs.time_elim, 2)
         hyb.exact_scan = int(EXACT)
         hyb.delta0, hyb.eta0 = float(knobs.delta0), float(knobs.eta0)
-        neg = np.stack([per_value(eps_rows(e, nx), lambda v: -v) for e in eps_list])
-        e2 = np.stack([per_value(eps_rows(e, nx), lambda v: v**2) for e in eps_list])
+        neg = np.stack([_eps_row(e, nx, "neg") for e in eps_list])
+        e2 = np.stack([_eps_row(e, nx, "sq") for e in eps_list])
         dneg, de2 = self.t(neg), self.t(e2)
         hyb.neg_eps, hyb.eps2 = _ptr(dneg), _ptr(de2)
         keep += [dneg, de2]
         if knobs.adaptation and knobs.scale_remainder:
-            rs = self.t(np.stack([per_value(eps_cells(e, nx), lambda v: v**2) for e in eps_list]))
+            rs = self.t(np.stack([_eps_row(e, nx, "cellsq") for e in eps_list]))
             hyb.rscale = _ptr(rs)
             keep.append(rs)
         else:

@@ -79,10 +79,32 @@ class KineticStepParams:
             raise StabilityViolation(
                 f"dt={dt:.6e} exceeds stability bounds "
                 f"(parabolic {parabolic:.6e}, transport {transport:.6e})")
-        for e in eps_values(self.eps):
-            if _transport_amplification(dt, e, _lambda_transport(mesh, 0.0)) > 1.0 + 1e-9:
-                raise StabilityViolation(
-                    f"dt={dt:.6e} violates the relaxed transport condition at eps={e:g}")
+        # the same scalar rule per distinct eps; an eps(x) profile has thousands
+        # of values and every parareal window re-checks the same (eps, dt):
+        # the first offending value (or None) is memoised
+        lam = _lambda_transport(mesh, 0.0)
+        key = (_eps_key(self.eps), dt, lam)
+        hit = _CHECKS.get(key)
+        if hit is None or hit[0] is not self.eps:
+            bad = None
+            for e in eps_values(self.eps):
+                if _transport_amplification(dt, e, lam) > 1.0 + 1e-9:
+                    bad = e
+                    break
+            hit = _CHECKS[key] = (self.eps, bad)
+            while len(_CHECKS) > 256:
+                _CHECKS.pop(next(iter(_CHECKS)))
+        if hit[1] is not None:
+            raise StabilityViolation(
+                f"dt={dt:.6e} violates the relaxed transport condition at eps={hit[1]:g}")
+
+
+_CHECKS: dict = {}    # (eps, dt, lambda) -> (eps, first offending eps or None)
+_STABLE: dict = {}    # (eps, mesh constants, knobs) -> (eps, dt)
+
+
+def _eps_key(eps):
+    return ("profile", id(eps)) if isinstance(eps, EpsProfile) else float(eps)
 
 
 def _lambda_transport(mesh: PhaseMesh, e_max: float) -> float:
@@ -115,9 +137,18 @@ def _stable_dt_scalar(mesh, eps, e_max, cfl_safety, theta, transport_safety):
 
 def stable_dt(mesh: PhaseMesh, eps, e_max: float = 0.0, cfl_safety: float = 0.9,
               theta: float = 0.9, transport_safety: float = 0.5) -> float:
-    """kinetic.py:107-138; for an EpsProfile the minimum over its values."""
-    return min(_stable_dt_scalar(mesh, e, e_max, cfl_safety, theta, transport_safety)
-               for e in eps_values(eps))
+    """kinetic.py:107-138; for an EpsProfile the minimum over its values
+    (memoised per profile: the same scalar bisection per distinct value)."""
+    key = (_eps_key(eps), mesh.dx, mesh.v_star, mesh.vgrid.m2, mesh.vgrid.dvx, float(e_max),
+           cfl_safety, theta, transport_safety)
+    hit = _STABLE.get(key)
+    if hit is None or hit[0] is not eps:
+        dt = min(_stable_dt_scalar(mesh, e, e_max, cfl_safety, theta, transport_safety)
+                 for e in eps_values(eps))
+        hit = _STABLE[key] = (eps, dt)
+        while len(_STABLE) > 256:
+            _STABLE.pop(next(iter(_STABLE)))
+    return hit[1]
 
 
 def kinetic_step(state, p: KineticStepParams, mesh: PhaseMesh, rho_bar: float,
