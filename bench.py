@@ -796,7 +796,7 @@ def v3_default_grid(peak, nx=128, B=37, steps=20):
                       f"{steps} kinetic steps, eps=0.5, device-resident",
             "value": val, "unit": "cell-updates/s", "ms": ms,
             "roofline_frac": val * 16 / (peak * 1e9),
-            "layout": "one CTA per row" if layout == 2 else "warp per row"}
+            "layout": {2: f"one CTA per row, clusters of {C}", 3: f"one CTA per row, software groups of {C}"}.get(layout, "warp per row")}
 
 
 if __name__ == "__main__":

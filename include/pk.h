@@ -121,7 +121,8 @@ int32_t pk_count_rows(pk_ctx* ctx, void* dev_counts);
  * slices per cluster, out[2] 1 when the slice vectors were kept in shared
  * memory, out[3] 1 when the group was a software group (cooperative launch,
  * moments through global memory) rather than a hardware cluster, 2 when big
- * 1D-3V rows ran one CTA per row. */
+ * 1D-3V rows ran one CTA per row in hardware clusters, 3 when they ran one
+ * CTA per row in software groups. */
 int32_t pk_fine_last_launch(pk_ctx* ctx, int32_t out[4]);
 
 /* --- fine propagator F --------------------------------------------------

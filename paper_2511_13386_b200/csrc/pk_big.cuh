@@ -100,7 +100,7 @@ __device__ __forceinline__ void big_row_moments(const double* row, const MeshDev
 
 // lifting.py:63-105 for one row, written into dst: g = xi M (-eps J)
 // [+ (eps^2 w) drift] [+ (eps^2 M) R_if]; two zero-mass projections.
-__device__ void big_row_lift(double* dst, const LiftRow& L, int order, int higher, int project,
+static __device__ void big_row_lift(double* dst, const LiftRow& L, int order, int higher, int project,
                              const MeshDev& m, double* scr, int lane) {
   const int nv = m.nv;
   for (int c = lane; c < nv; c += 32) {

@@ -32,6 +32,14 @@
 
 namespace cg = cooperative_groups;
 
+// The file compiles either as one translation unit or, for a parallel build
+// (build.py), once per PK_FINE_PART: part 0 holds the standalone operators and
+// the dispatcher, parts 1.. one fine_kernel layout each.
+#ifndef PK_FINE_PART
+#define PK_FINE_PART -1
+#endif
+#define PK_IN_PART(n) (PK_FINE_PART < 0 || PK_FINE_PART == (n))
+
 namespace pk {
 
 // ---------------------------------------------------------------------------
@@ -246,7 +254,7 @@ __device__ __forceinline__ double stencil_reg(const double (&w)[7], const MeshDe
 // running carry across rounds; the warp offsets and -- folded into the same
 // barrier -- sum(E) for the zero-mean gauge come from per-warp partials
 // (sum_w C_w off_w + A_w).  Works on shared or global vectors alike.
-__device__ bool slice_field_fast(const MeshDev& m, const double* __restrict__ rho, double rb,
+static __device__ bool slice_field_fast(const MeshDev& m, const double* __restrict__ rho, double rb,
                                  double* __restrict__ E_out, double rtol, double* red) {
   const int nx = m.nx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -347,7 +355,7 @@ __device__ bool slice_field_fast(const MeshDev& m, const double* __restrict__ rh
 // partials meet in the leader's shared memory through DSMEM (two cluster
 // barriers), so each pass is nx / (C x warps) cells per warp instead of one
 // CTA walking all of them.  Same arithmetic shape as slice_field_fast.
-__device__ bool cluster_field_fast(const MeshDev& m, const double* __restrict__ rho, double rb,
+static __device__ bool cluster_field_fast(const MeshDev& m, const double* __restrict__ rho, double rb,
                                    double* __restrict__ E_out, double rtol, double* red,
                                    int rank, int C) {
   const int nx = m.nx;
@@ -474,7 +482,7 @@ __device__ bool cluster_field_fast(const MeshDev& m, const double* __restrict__ 
   return true;
 }
 
-__device__ bool slice_field(const MeshDev& m, const double* rho, double rb, double* src,
+static __device__ bool slice_field(const MeshDev& m, const double* rho, double rb, double* src,
                             double* E_out, double rtol, int exact_scan, bool on_chip,
                             const Smem& sm, long long* dbg = nullptr, bool src_ready = false,
                             double* mean_out = nullptr) {
@@ -606,7 +614,7 @@ __device__ __forceinline__ double flux_J(double r, double rn, double e, double d
 }
 
 // Block-wide exclusive scan of per-thread counts; returns the total.
-__device__ int block_excl_scan(int v, int* out_prefix, int* sbuf) {
+static __device__ int block_excl_scan(int v, int* out_prefix, int* sbuf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   int inc = v;
 #pragma unroll
@@ -722,7 +730,7 @@ __device__ __forceinline__ KSeg kseg_shfl_up(const KSeg& x, int o) {
 
 // Block-wide exclusive scan of KSeg (thread order); returns the total.
 // `wt`: 4 * nwarp ints of shared memory.  One barrier.
-__device__ KSeg kseg_block_scan(const KSeg& mine, KSeg& excl, int* wt) {
+static __device__ KSeg kseg_block_scan(const KSeg& mine, KSeg& excl, int* wt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const KSeg id = {0, 0, 0, 0};
   KSeg inc = mine;
@@ -1491,7 +1499,7 @@ __device__ bool prepare_step(const FineArgs& a, const SliceView& v, const Smem& 
 
 // Slice phase after step s: masked rho update and field.  Returns false on a
 // solvability violation.  kc/ki are the labels the step ran with.
-__device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int ph, int step,
+static __device__ bool finish_step(const FineArgs& a, SliceView& v, const Smem& sm, int ph, int step,
                             const Par& Q) {
   const MeshDev& m = a.m;
   const int nx = m.nx;
@@ -2215,7 +2223,7 @@ __device__ void micro_phase_pc(const FineArgs& a, const SliceView& v, int ph, co
 }
 
 // Micro phase, generic layout (any nv <= 256, no TMA): direct row loads.
-__device__ void micro_phase_gen(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
+static __device__ void micro_phase_gen(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                 const double* gin, double* gout, int wg, int nwg) {
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
@@ -2253,7 +2261,7 @@ __device__ void micro_phase_gen(const FineArgs& a, const SliceView& v, const Sme
 }
 
 // Micro phase, big rows (pk_big.cuh): one warp per listed row.
-__device__ void micro_phase_big(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
+static __device__ void micro_phase_big(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                 const double* gin, double* gout, int wg, int nwg) {
   const MeshDev& m = a.m;
   const int nx = m.nx, nv = m.nv;
@@ -2323,7 +2331,7 @@ struct BigcCnt {
   uint32_t q[3];
 };
 
-__device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
+static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                  const double* gin, double* gout, int crank, int C, double* rbuf,
                                  const double* sxi, uint64_t* mbar, BigcCnt& cnt) {
   constexpr int S = BIGC_S, X = BIGC_NXI, NM = 16, HX = X / 2;
@@ -2650,7 +2658,7 @@ __device__ void prologue_rows(const FineArgs& a, const SliceView& v, const Smem&
 // Window-start lift scalars (parareal.py:171-178: lift(rho_in, E) with
 // dE_dt = None, i.e. dtE_c = 0), written to cluster-shared arrays (global)
 // for every CTA's prologue row pass.
-__device__ bool lift_scalars(const FineArgs& a, const SliceView& v, const Smem& sm, double* out_J,
+static __device__ bool lift_scalars(const FineArgs& a, const SliceView& v, const Smem& sm, double* out_J,
                              double* out_drift, double* out_Rif) {
   const MeshDev& m = a.m;
   const int nx = m.nx, tid = threadIdx.x, nt = blockDim.x;
@@ -3138,6 +3146,7 @@ __global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128)) ? 1 : 2)
 // Standalone operators: lift (lifting.py:38-105) and solve_field
 // (poisson.py:21-54) over B slices, one CTA per slice.
 
+#if PK_IN_PART(0)
 template <int T>
 __global__ void __launch_bounds__(256) lift_kernel(const LiftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -3238,6 +3247,8 @@ __global__ void __launch_bounds__(256) field_kernel(const FieldArgs a) {
   }
 }
 
+#endif  // PK_IN_PART(0)
+
 // ---------------------------------------------------------------------------
 // Host-side launch.
 
@@ -3265,11 +3276,14 @@ static size_t local_smem(int nx, int adaptation) {
 }
 
 // layout of the calling thread's last fine launch (pk_fine_last_launch)
-static thread_local int last_launch[4] = {0, 0, 0, 0};
+extern thread_local int last_launch[4];
+#if PK_IN_PART(0)
+thread_local int last_launch[4] = {0, 0, 0, 0};
 
 void fine_last_launch(int out[4]) {
   for (int i = 0; i < 4; ++i) out[i] = last_launch[i];
 }
+#endif
 
 template <int T, int S, int G, int NT, bool AD>
 static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
@@ -3388,6 +3402,69 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   }
   a.kps = 1;
   a.sg = 0;
+  if constexpr (T < 0) {
+    // Big rows, one CTA per row and one CTA per SM: the cluster size that
+    // keeps every cluster resident.  GPC packing admits fewer clusters than
+    // num_sms / C (37 slices x 4 CTAs = 148 CTAs run as two waves, 32 + 5);
+    // a second wave doubles the launch.  Cost of a size: waves x rows per CTA.
+    // All-kinetic slices with on-chip vectors may run as software groups
+    // instead (cooperative launch, moments through global memory as for the
+    // G8 layouts): no GPC limit, every SM busy.
+    if (a.bigc && autok) {
+      static size_t b_smem = 0;
+      static int b_max[17];
+      if (b_smem != smem) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        for (int cc = 1; cc <= 16; ++cc) {
+          cudaLaunchConfig_t qc = {};
+          qc.gridDim = dim3(cc);
+          qc.blockDim = dim3(NT);
+          qc.dynamicSmemBytes = smem;
+          cudaLaunchAttribute qa[1];
+          qa[0].id = cudaLaunchAttributeClusterDimension;
+          qa[0].val.clusterDim.x = cc;
+          qa[0].val.clusterDim.y = 1;
+          qa[0].val.clusterDim.z = 1;
+          qc.attrs = qa;
+          qc.numAttrs = 1;
+          int n = 0;
+          if (cudaOccupancyMaxActiveClusters(&n, kern, &qc) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+          }
+          b_max[cc] = n;
+        }
+        b_smem = smem;
+        if (dbg_packing) {
+          fprintf(stderr, "pk big rows: smem %zu, max active clusters:", smem);
+          for (int cc = 1; cc <= 16; ++cc) fprintf(stderr, " %d:%d", cc, b_max[cc]);
+          fprintf(stderr, "\n");
+        }
+      }
+      auto rows = [&](int cc) { return (long long)((a.m.nx + cc - 1) / cc); };
+      long long best = -1;
+      for (int cc = 1; cc <= 16; ++cc) {
+        if (b_max[cc] <= 0 || a.m.nx < 2 * cc) continue;
+        const long long cost = (long long)((a.B + b_max[cc] - 1) / b_max[cc]) * rows(cc);
+        if (best < 0 || cost < best) {
+          best = cost;
+          C = cc;
+        }
+      }
+      static const bool no_sg = getenv("PK_NO_SG") != nullptr;
+      if (!AD && !no_sg && a.local_smem && best >= 0)
+        for (int cc = 2; cc <= 16; ++cc) {
+          if ((long long)a.B * cc > num_sms || a.m.nx < 2 * cc) continue;
+          // (the group barrier costs more than a cluster barrier: strictly fewer rows)
+          if (rows(cc) < best) {
+            best = rows(cc);
+            C = cc;
+            a.sg = cc;
+          }
+        }
+    }
+  }
   if constexpr (!AD && G > 0) {
     // More slices than SMs (one CTA per slice, some SMs with one CTA and some
     // with two): pack K slices into clusters of C > K CTAs so that every CTA
@@ -3470,7 +3547,7 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   last_launch[0] = C;
   last_launch[1] = a.kps;
   last_launch[2] = a.local_smem;
-  last_launch[3] = sg ? 1 : (a.bigc ? 2 : 0);
+  last_launch[3] = a.bigc ? (sg ? 3 : 2) : (sg ? 1 : 0);
   if (sg) {
     e = cudaMemsetAsync(a.sg_cnt, 0, (size_t)((a.B + a.kps - 1) / a.kps) * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
@@ -3505,6 +3582,62 @@ static cudaError_t launch_T(const FineArgs& a, int C, cudaStream_t st) {
                       : launch_TA<T, S, G, NT, false>(a, C, st);
 }
 
+// one fine_kernel layout (both adaptation modes) per part
+#define PK_LAYOUT(n, name, ...)                                           \
+  cudaError_t name(const FineArgs& a, int C, cudaStream_t st);            \
+  PK_LAYOUT_BODY_##n(name, __VA_ARGS__)
+#define PK_LAYOUT_DEF(name, ...) \
+  cudaError_t name(const FineArgs& a, int C, cudaStream_t st) { return launch_T<__VA_ARGS__>(a, C, st); }
+#if PK_IN_PART(0)
+#define PK_LAYOUT_BODY_0(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_0(name, ...)
+#endif
+#if PK_IN_PART(1)
+#define PK_LAYOUT_BODY_1(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_1(name, ...)
+#endif
+#if PK_IN_PART(2)
+#define PK_LAYOUT_BODY_2(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_2(name, ...)
+#endif
+#if PK_IN_PART(3)
+#define PK_LAYOUT_BODY_3(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_3(name, ...)
+#endif
+#if PK_IN_PART(4)
+#define PK_LAYOUT_BODY_4(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_4(name, ...)
+#endif
+#if PK_IN_PART(5)
+#define PK_LAYOUT_BODY_5(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_5(name, ...)
+#endif
+#if PK_IN_PART(6)
+#define PK_LAYOUT_BODY_6(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_6(name, ...)
+#endif
+#if PK_IN_PART(7)
+#define PK_LAYOUT_BODY_7(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_7(name, ...)
+#endif
+PK_LAYOUT(0, fine_generic, 0, 1, 0, 256)      // generic rows (<= 256 nodes)
+PK_LAYOUT(1, fine_big, -1, 1, 0, 256)         // big 1D-3V rows
+PK_LAYOUT(2, fine_g8_64w, 2, 16, 4, 256)      // nv = 64, G8, 8 warps
+PK_LAYOUT(3, fine_g8_64, 2, 16, 4, 128)       // nv = 64, G8, 4 warps
+PK_LAYOUT(4, fine_g8_128w, 4, 14, 8, 256)     // nv = 128, G8, 8 warps
+PK_LAYOUT(5, fine_g8_128, 4, 14, 8, 128)      // nv = 128, G8, 4 warps
+PK_LAYOUT(6, fine_gs_256, 8, 20, -4, 256)     // nv = 256, producer/consumer
+PK_LAYOUT(7, fine_tma_512, 16, 3, 0, 256)     // nv = 512
+
+#if PK_IN_PART(0)
 template <int T>
 static cudaError_t launch_lift_T(const LiftArgs& a, cudaStream_t st) {
   const size_t smem = T < 0 ? (kThreads / 32) * (size_t)BIG_SCR * 8
@@ -3641,11 +3774,11 @@ cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
 
 cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   if (a.m.nvyz > 1) {  // 1D-3V rows: generic layout up to 256 nodes, big rows beyond
-    if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
-    return launch_T<-1, 1, 0, 256>(a, C, st);
+    if (a.m.nv <= 32 * GT) return fine_generic(a, C, st);
+    return fine_big(a, C, st);
   }
   if ((a.m.nv == 64 || a.m.nv == 128) && !a.m.mirror)  // G8 needs the mirrored grid
-    return launch_T<0, 1, 0, 256>(a, C, st);
+    return fine_generic(a, C, st);
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -3663,21 +3796,22 @@ cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
   switch (a.m.nv) {
     // producer/consumer GS pipeline: 7 consumer warps + 1 producer warp
     case 64:  // G8 per-warp rings, 4 warps (8 at one CTA per SM)
-      if (wide) e = launch_T<2, 16, 4, 256>(a, C, st);
-      if (e == cudaErrorNotSupported) e = launch_T<2, 16, 4, 128>(a, C, st);
+      if (wide) e = fine_g8_64w(a, C, st);
+      if (e == cudaErrorNotSupported) e = fine_g8_64(a, C, st);
       return e;
     case 128:
-      if (wide) e = launch_T<4, 14, 8, 256>(a, C, st);
-      if (e == cudaErrorNotSupported) e = launch_T<4, 14, 8, 128>(a, C, st);
+      if (wide) e = fine_g8_128w(a, C, st);
+      if (e == cudaErrorNotSupported) e = fine_g8_128(a, C, st);
       return e;
       // (8 warps at two CTAs per SM, <= 128 registers: no spills, but the micro
       // loop loses its ILP and the step takes 1.6x longer)
-    case 256: return launch_T<8, 20, -4, 256>(a, C, st);
-    case 512: return launch_T<16, 3, 0, 256>(a, C, st);
+    case 256: return fine_gs_256(a, C, st);
+    case 512: return fine_tma_512(a, C, st);
     default:
-      if (a.m.nv <= 32 * GT) return launch_T<0, 1, 0, 256>(a, C, st);
+      if (a.m.nv <= 32 * GT) return fine_generic(a, C, st);
       return cudaErrorInvalidValue;
   }
 }
+#endif  // PK_IN_PART(0)
 
 }  // namespace pk

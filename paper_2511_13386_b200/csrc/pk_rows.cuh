@@ -305,7 +305,7 @@ __device__ void fast_lift_row(double (&g)[T], const LiftRow& L, int order, int h
   }
 }
 
-__device__ void gen_lift_row(double (&g)[GT], const LiftRow& L, int order, int higher, int project,
+static __device__ void gen_lift_row(double (&g)[GT], const LiftRow& L, int order, int higher, int project,
                              const Smem& sm, const MeshDev& m, double* wrow, int lane) {
   const int nv = m.nv;
 #pragma unroll

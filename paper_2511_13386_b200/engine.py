@@ -293,7 +293,8 @@ class Device:
     def last_launch(self):
         """Layout of this thread's last fine launch: (CTAs per cluster or group,
         slices per cluster, slice vectors in shared memory, kind: 0 hardware
-        cluster, 1 software group, 2 big rows one CTA per row)."""
+        cluster, 1 software group, 2 big rows one CTA per row in hardware clusters,
+        3 the same in software groups)."""
         out = (C.c_int32 * 4)()
         self._rc(self.lib.pk_fine_last_launch(self.ctx, out), "pk_fine_last_launch")
         return out[0], out[1], bool(out[2]), int(out[3])

@@ -173,6 +173,6 @@ def test_big_rows_repeat_bitwise():
             s.synchronize()
         outs.append((ens.rho.cpu().numpy(), ens.g.cpu().numpy()))
         torch.cuda.synchronize()
-    assert ens.dev.last_launch()[3] == 2 or "PK_NO_BIGC" in os.environ
+    assert ens.dev.last_launch()[3] in (2, 3) or "PK_NO_BIGC" in os.environ
     for o in outs[1:]:
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
