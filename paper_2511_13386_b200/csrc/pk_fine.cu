@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "../../include/pk.h"
 #include "pk_rows.cuh"
@@ -2353,8 +2354,8 @@ static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, c
   double Ml[NM], Mh[NM];
 #pragma unroll
   for (int u = 0; u < NM; ++u) {
-    Ml[u] = __ldg(m.M + jx * S + col0 + 8 * u);
-    Mh[u] = __ldg(m.M + jm * S + col0 + 8 * u);
+    Ml[u] = __ldg(m.M + jx * S + col0 + 8 * (u ^ (l & 1)));  // (node order of the bank swizzle)
+    Mh[u] = __ldg(m.M + jm * S + col0 + 8 * (u ^ (l & 1)));
   }
   auto rowid = [&](int p) { return dense ? p : __ldcg(v.klist + p); };
   auto coef = [&](int i) {
@@ -2372,19 +2373,49 @@ static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, c
     mbar_expect_tx(mb, bytes);
     bulk_g2s(dst, src, bytes, mb);
   };
+  // Bank swizzle.  The two leaves of a half warp (column blocks 0 and 1 of
+  // one plane) sit 1 KB apart: the same 16 banks, a 2-way conflict on every
+  // load.  Lanes of block 1 therefore visit their 16 columns in the order
+  // 1, 0, 3, 2, ... (node u ^ odd at loop index u: the other 16 banks), and
+  // the fold terms of a pair are added in node order afterwards -- the same
+  // chain.  Staged data is read through the shared window (ld.shared, 32-bit
+  // addresses; [0] for even u, [1] for odd u, + 64 u bytes).
+  const int odd = l & 1;
+  auto node = [&](int u) { return u ^ odd; };
+  struct Addr {
+    uint32_t e, o;
+  };
+  auto addr = [&](const double* base) {  // base: the thread's column k of a staged plane
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(base);
+    return Addr{b + (odd ? 64u : 0u), b - (odd ? 64u : 0u)};
+  };
+  auto lds = [&](const Addr& a_, int u) {
+    double x;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(((u & 1) ? a_.o : a_.e) + 64u * (uint32_t)u));
+    return x;
+  };
   // The node update of plane jx (lower, xi < 0) and jm (upper, xi > 0) for
-  // u = 0..15: g/gb/gf the node and its xi neighbours, xn the x neighbour.
-  // Leaves the outputs in yl/yh and the fold-term accumulators in a1/a2.
-  auto row_update = [&](const RowCoef& rc, auto lo_at, auto hi_at, double (&yl)[NM],
-                        double (&yh)[NM], double& a1, double& a2) {
+  // u = 0..15: g/gb/gf the node and its xi neighbours, xn the x neighbour
+  // (staged, or xa/xb when XS is false).  Stores the outputs of row i and
+  // leaves the fold-term accumulators in a1/a2.
+  auto row_update = [&](const RowCoef& rc, auto XS, const Addr& gl, const Addr& bl, const Addr& fl,
+                        const Addr& xl_, const Addr& gh, const Addr& bh, const Addr& fh,
+                        const Addr& xh_, const double (&xa)[NM], const double (&xb)[NM], int i,
+                        double& a1, double& a2) {
+    // (outputs stored as they are formed: no output registers held over the row)
+    double* const ol = gout + (size_t)i * nv + jx * S + col0;
+    double* const oh = gout + (size_t)i * nv + jm * S + col0;
     const double Ep = rc.vsg > 0 ? rc.vco : 0.0;
     const double Em = rc.vsg < 0 ? rc.vco : 0.0;
+    double f1[2], f2[2];
 #pragma unroll
     for (int u = 0; u < NM; ++u) {
-      double g, gb, gf, xn;
-      lo_at(u, g, gb, gf, xn);
       double lo, hi;
       {  // plane jx, xi < 0: x-upwind from row i+1; zero xi-inflow below plane 0
+        const double g = lds(gl, u);
+        const double gb = jx > 0 ? lds(bl, u) : 0.0;
+        const double gf = lds(fl, u);
+        const double xn = decltype(XS)::value ? lds(xl_, u) : xa[u];
         double w = xl * (xn - g);
         w = qdiv(w, dx, rdx);
         const double dm = jx == 0 ? g : g - gb;
@@ -2396,8 +2427,11 @@ static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, c
         const double forcing = w + (xl * Mc) * rc.J;
         lo = rc.k1 * g - rc.k2 * forcing;
       }
-      hi_at(u, g, gb, gf, xn);
       {  // plane 31 - jx, xi > 0: x-upwind from row i-1; zero inflow above plane 31
+        const double g = lds(gh, u);
+        const double gb = lds(bh, u);
+        const double gf = jm + 1 < X ? lds(fh, u) : 0.0;
+        const double xn = decltype(XS)::value ? lds(xh_, u) : xb[u];
         double w = xh * (g - xn);
         w = qdiv(w, dx, rdx);
         const double dm = g - gb;  // (jm - 1 >= 15 >= 0)
@@ -2409,27 +2443,25 @@ static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, c
         const double forcing = w + (xh * Mc) * rc.J;
         hi = rc.k1 * g - rc.k2 * forcing;
       }
-      yl[u] = lo;
-      yh[u] = hi;
-      // fold terms (q(j) + q(mirror j)), accumulated in leaf order
-      const double f1 = xl * lo + xh * hi;
-      a1 = u == 0 ? f1 : a1 + f1;
-      if (sq) {
-        const double f2 = lo * lo + hi * hi;
-        a2 = u == 0 ? f2 : a2 + f2;
+      __stcg(ol + 8 * node(u), lo);
+      __stcg(oh + 8 * node(u), hi);
+      // fold terms (q(j) + q(mirror j)), accumulated in leaf (node) order
+      f1[u & 1] = xl * lo + xh * hi;
+      if (sq) f2[u & 1] = lo * lo + hi * hi;
+      if (u & 1) {
+        const double s0 = odd ? f1[1] : f1[0], s1 = odd ? f1[0] : f1[1];
+        a1 = u == 1 ? s0 : a1 + s0;
+        a1 = a1 + s1;
+        if (sq) {
+          const double t0 = odd ? f2[1] : f2[0], t1 = odd ? f2[0] : f2[1];
+          a2 = u == 1 ? t0 : a2 + t0;
+          a2 = a2 + t1;
+        }
       }
     }
   };
-  // stores, leaf butterflies, the tree over the leaves and the moments of row i
-  auto row_finish = [&](int i, const double (&yl)[NM], const double (&yh)[NM], double a1,
-                        double a2) {
-    double* ol = gout + (size_t)i * nv + jx * S + col0;
-    double* oh = gout + (size_t)i * nv + jm * S + col0;
-#pragma unroll
-    for (int u = 0; u < NM; ++u) {
-      __stcg(ol + 8 * u, yl[u]);
-      __stcg(oh + 8 * u, yh[u]);
-    }
+  // leaf butterflies, the tree over the leaves and the moments of row i
+  auto row_finish = [&](int i, double a1, double a2) {
     a1 = a1 + __shfl_xor_sync(FULL, a1, 1);
     a1 = a1 + __shfl_xor_sync(FULL, a1, 2);
     a1 = a1 + __shfl_xor_sync(FULL, a1, 4);
@@ -2499,28 +2531,16 @@ static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, c
       const double* Up = wait_u(q);      // row i-1, upper half
       const double* Uc = wait_u(q + 1);  // own upper half
       const double* rl = Lc + jx * S + col0;
-      const double* rlf = jx + 1 < HX ? rl + S : Uc + col0;  // plane jx + 1
-      const double* xl_ = Ln + jx * S + col0;
       const double* rh = Uc + (jm - HX) * S + col0;
-      const double* rhb = jm > HX ? rh - S : Lc + (HX - 1) * S + col0;  // plane jm - 1
-      const double* xh_ = Up + (jm - HX) * S + col0;
-      double yl[NM], yh[NM], a1 = 0.0, a2 = 0.0;
-      row_update(
-          rc,
-          [&](int u, double& g, double& gb, double& gf, double& xn) {
-            g = rl[8 * u];
-            gb = jx > 0 ? rl[8 * u - S] : 0.0;
-            gf = rlf[8 * u];
-            xn = xl_[8 * u];
-          },
-          [&](int u, double& g, double& gb, double& gf, double& xn) {
-            g = rh[8 * u];
-            gb = rhb[8 * u];
-            gf = jm + 1 < X ? rh[8 * u + S] : 0.0;
-            xn = xh_[8 * u];
-          },
-          yl, yh, a1, a2);
-      row_finish(i, yl, yh, a1, a2);
+      const Addr gl = addr(rl), bl = addr(rl - S);
+      const Addr fl = addr(jx + 1 < HX ? rl + S : Uc + col0);  // plane jx + 1
+      const Addr xl_ = addr(Ln + jx * S + col0);
+      const Addr gh = addr(rh), fh = addr(rh + S);
+      const Addr bh = addr(jm > HX ? rh - S : Lc + (HX - 1) * S + col0);  // plane jm - 1
+      const Addr xh_ = addr(Up + (jm - HX) * S + col0);
+      double a1 = 0.0, a2 = 0.0;
+      row_update(rc, std::true_type{}, gl, bl, fl, xl_, gh, bh, fh, xh_, Ml, Mh, i, a1, a2);
+      row_finish(i, a1, a2);
       // (after row_finish's barrier) slots of L_q and U_q are free: L_{q+3}, U_{q+3}
       if (tid == 0) {
         if (q + 3 <= n) issue_l(q + 3);
@@ -2563,35 +2583,86 @@ static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, c
     double xa[NM], xb[NM];
 #pragma unroll
     for (int u = 0; u < NM; ++u) {
-      xa[u] = __ldcg(gnl + 8 * u);
-      xb[u] = __ldcg(gph + 8 * u);
+      xa[u] = __ldcg(gnl + 8 * node(u));
+      xb[u] = __ldcg(gph + 8 * node(u));
     }
     mbar_wait(mbar + (Q & 1), (Q >> 1) & 1);
     const double* rl = rb + jx * S + col0;
     const double* rh = rb + jm * S + col0;
-    double yl[NM], yh[NM], a1 = 0.0, a2 = 0.0;
-    row_update(
-        rc,
-        [&](int u, double& g, double& gb, double& gf, double& xn) {
-          g = rl[8 * u];
-          gb = jx > 0 ? rl[8 * u - S] : 0.0;
-          gf = rl[8 * u + S];
-          xn = xa[u];
-        },
-        [&](int u, double& g, double& gb, double& gf, double& xn) {
-          g = rh[8 * u];
-          gb = rh[8 * u - S];
-          gf = jm + 1 < X ? rh[8 * u + S] : 0.0;
-          xn = xb[u];
-        },
-        yl, yh, a1, a2);
-    row_finish(i, yl, yh, a1, a2);
+    const Addr gl = addr(rl), bl = addr(rl - S), fl = addr(rl + S);
+    const Addr gh = addr(rh), bh = addr(rh - S), fh = addr(rh + S);
+    double a1 = 0.0, a2 = 0.0;
+    row_update(rc, std::false_type{}, gl, bl, fl, gl, gh, bh, fh, gh, xa, xb, i, a1, a2);
+    row_finish(i, a1, a2);
     if (p + 2 < p1) issue(q + 2, i_n2);  // (the staged row was only read: no proxy fence)
     i_cur = i_nxt;
     i_nxt = i_n2;
     rc = rn;
   }
   qbase += (uint32_t)(p1 - p0);
+}
+
+// Prologue row pass of the one-CTA-per-row big-row layout without a lift:
+// copy the input rows into the step-0 input buffer and form their moments in
+// micro_phase_bigc's thread layout (same leaves, butterflies and tree), every
+// CTA of the cluster / group its share of the rows.
+static __device__ void prologue_rows_bigc(const FineArgs& a, const SliceView& v, const Smem& sm,
+                                          double* gin0, const double* sxi, int crank, int C) {
+  constexpr int S = BIGC_S, X = BIGC_NXI, NM = 16;
+  const MeshDev& m = a.m;
+  const int nx = m.nx, nv = m.nv;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int l = tid >> 3, k = lane & 7;
+  const int jx = l >> 1, jm = X - 1 - jx;
+  const int col0 = (l & 1) * 128 + k;
+  const double xl = sxi[jx], xh = sxi[jm];
+  const int p0 = (int)(((long long)crank * nx) / C), p1 = (int)(((long long)(crank + 1) * nx) / C);
+  const bool cp = gin0 != v.ga;
+  for (int i = p0; i < p1; ++i) {
+    const double* rl = v.ga + (size_t)i * nv + jx * S + col0;
+    const double* rh = v.ga + (size_t)i * nv + jm * S + col0;
+    double lo[NM], hi[NM];
+#pragma unroll
+    for (int u = 0; u < NM; ++u) {
+      lo[u] = __ldcg(rl + 8 * u);
+      hi[u] = __ldcg(rh + 8 * u);
+    }
+    double a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < NM; ++u) {
+      if (cp) {
+        __stcg(gin0 + (size_t)i * nv + jx * S + col0 + 8 * u, lo[u]);
+        __stcg(gin0 + (size_t)i * nv + jm * S + col0 + 8 * u, hi[u]);
+      }
+      const double f1 = xl * lo[u] + xh * hi[u];
+      const double f2 = lo[u] * lo[u] + hi[u] * hi[u];
+      a1 = u == 0 ? f1 : a1 + f1;
+      a2 = u == 0 ? f2 : a2 + f2;
+    }
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {
+      a1 = a1 + __shfl_xor_sync(FULL, a1, d);
+      a2 = a2 + __shfl_xor_sync(FULL, a2, d);
+    }
+    if (k == 0) {
+      sm.red[l] = a1;
+      sm.red[32 + l] = a2;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double r1 = sm.red[lane], r2 = sm.red[32 + lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        r1 = r1 + __shfl_xor_sync(FULL, r1, d);
+        r2 = r2 + __shfl_xor_sync(FULL, r2, d);
+      }
+      if (tid == 0) {
+        v.fl_w[i] = r1 * m.dv3;
+        v.sq_w[i] = r2 * m.dv3;
+      }
+    }
+    __syncthreads();  // sm.red is rewritten by the next row
+  }
 }
 
 // Prologue row pass: (optionally lift and) copy the input rows into the
@@ -2984,7 +3055,9 @@ __global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128)) ? 1 : 2)
   }
   barrier();
   if (K == 1 && __ldcg(abort_flag)) return;
-  if (K == 1)
+  if (T < 0 && a.bigc && !lift0 && K == 1)
+    prologue_rows_bigc(a, v, sm, buf(0), ring + 3 * (size_t)nv, crank, C);
+  else if (K == 1)
     prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, wg, nwg);
   else if (leader && !__ldcg(abort_flag))  // several slices: each owner's warps
     prologue_rows<T>(a, v, sm, buf(0), lift0, v.gJ, v.dco, v.vco, warp, nwpc);
