@@ -228,7 +228,9 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
 // eight operands are loaded first (into n*), then acc += c_k and the running
 // sum is stored, k = 0..7.  One block keeps the compiler from sinking the
 // loads next to their adds, which it does under register pressure (kernels
-// capped at 128 registers) and which doubles the chain's cost.
+// capped at 128 registers) and which doubles the chain's cost.  (Volatile
+// accesses, which ptxas keeps in program order, cost 1.5 cycles per element:
+// tools/cumsum_bench2.cu.)
 #define PK_CS8(acc, c, nn, lda, sta)                                                      \
   asm volatile(                                                                            \
       "{\n\t"                                                                              \
@@ -263,11 +265,33 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
 // Keep the operand a plain load: an extra DADD per element (e.g. a fused
 // subtrahend) doubles the cost.  Thread 0 only.  `init`: the chain's carry
 // (-0.0 starts np.cumsum: -0 + x == x for every x).
+static __device__ __forceinline__ void smem_cumsum_body(uint32_t s, uint32_t d, int n, double init);
+
 __device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int n,
                                             double init = -0.0) {
   if (threadIdx.x != 0) return;
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(src);
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  smem_cumsum_body((uint32_t)__cvta_generic_to_shared(src),
+                          (uint32_t)__cvta_generic_to_shared(dst), n, init);
+}
+
+// The same chain as a function call, for kernels under register pressure:
+// compiled on its own it keeps the schedule it has in isolation (9.0 cycles
+// per element, tools/cumsum_bench2.cu); inlined into the 128-register hybrid
+// kernels the same code ran at 12.5 (the block's loads and stores sharing
+// scoreboards with the chain operands).  Elsewhere the inlined form is the
+// faster one (8.5).
+static __device__ __noinline__ void smem_cumsum_chain(uint32_t s, uint32_t d, int n, double init) {
+  smem_cumsum_body(s, d, n, init);
+}
+
+__device__ __forceinline__ void smem_cumsum_call(const double* src, double* dst, int n,
+                                                 double init = -0.0) {
+  if (threadIdx.x != 0) return;
+  smem_cumsum_chain((uint32_t)__cvta_generic_to_shared(src), (uint32_t)__cvta_generic_to_shared(dst),
+                    n, init);
+}
+
+static __device__ __forceinline__ void smem_cumsum_body(uint32_t s, uint32_t d, int n, double init) {
   double acc = init;
   const int n2 = n - n % 16;
   if (n2 > 0) {
@@ -281,6 +305,7 @@ __device__ __forceinline__ void smem_cumsum(const double* src, double* dst, int 
       PK_CS8(acc, Bv, A, nxt, d + 8 * (i + 8));
     }
   }
+#pragma unroll 1
   for (int i = n2; i < n; ++i) {
     acc = acc + lds64(s + 8 * i);
     sts64(d + 8 * i, acc);

@@ -517,7 +517,7 @@ static __device__ bool slice_field(const MeshDev& m, const double* rho, double r
       for (int i = threadIdx.x; i < nx; i += blockDim.x) sc[i] = (rho[i] - rb) * m.dx - corr;
       __syncthreads();
       PK_TICK(2)
-      smem_cumsum(sc, sc, nx, -0.0);
+      smem_cumsum_call(sc, sc, nx, -0.0);
       __syncthreads();
       PK_TICK(3)
       const double mean =
@@ -534,7 +534,7 @@ static __device__ bool slice_field(const MeshDev& m, const double* rho, double r
       for (int i = threadIdx.x; i < len; i += blockDim.x)
         sc[i] = (rho[q0 + i] - rb) * m.dx - corr;
       __syncthreads();
-      smem_cumsum(sc, sc, len, carry);
+      smem_cumsum_call(sc, sc, len, carry);
       __syncthreads();
       carry = sc[len - 1];
       for (int i = threadIdx.x; i < len; i += blockDim.x) E_out[q0 + i] = sc[i];

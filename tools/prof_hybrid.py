@@ -83,6 +83,12 @@ def main():
               "zero %d, klist %d, kstream %d" % tuple(int(x) // ns for x in cc[16:25]))
         print("   rows/step: flipped %.1f, zeroed %.1f, kinetic %.1f"
               % tuple(float(x) / ns for x in cc[26:29]))
+        Cc = dev.last_launch()[0]
+        ncta = min(a.B * Cc, 1024)
+        smid = [int(x) for x in cc[34:34 + 3 * ncta:3]]
+        shared = len(smid) - len(set(smid))
+        print(f"   clusters of {Cc}: {ncta} CTAs on {len(set(smid))} SMs ({shared} CTAs share an SM); "
+              f"slice 0's CTAs on SMs {smid[:Cc]}")
 
 
 if __name__ == "__main__":
