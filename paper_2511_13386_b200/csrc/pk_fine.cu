@@ -2332,6 +2332,8 @@ struct BigcCnt {
   uint32_t q[3];
 };
 
+// SQ: the <g^2> row moment (adaptation on) is formed too
+template <bool SQ>
 static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, const Smem& sm, int ph,
                                  const double* gin, double* gout, int crank, int C, double* rbuf,
                                  const double* sxi, uint64_t* mbar, BigcCnt& cnt) {
@@ -2348,7 +2350,7 @@ static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, c
   const int l = tid >> 3, k = lane & 7;  // leaf, accumulator
   const int jx = l >> 1, jm = X - 1 - jx;
   const int col0 = (l & 1) * 128 + k;
-  const bool sq = a.adaptation != 0;
+  constexpr bool sq = SQ;
   const double xl = sxi[jx], xh = sxi[jm];
   const double dx = m.dx, rdx = m.rdx;
   double Ml[NM], Mh[NM];
@@ -2418,7 +2420,7 @@ static __device__ void micro_phase_bigc(const FineArgs& a, const SliceView& v, c
         const double xn = decltype(XS)::value ? lds(xl_, u) : xa[u];
         double w = xl * (xn - g);
         w = qdiv(w, dx, rdx);
-        const double dm = jx == 0 ? g : g - gb;
+        const double dm = g - gb;  // (gb = 0.0 below plane 0: g - 0.0 == g bitwise)
         w = w + dm * Ep;
         const double dp = gf - g;  // (jx + 1 <= 16 < X)
         w = w + dp * Em;
@@ -3137,7 +3139,7 @@ __global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128)) ? 1 : 2)
     else if constexpr (T == 0)
       micro_phase_gen(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
     else if (a.bigc)
-      micro_phase_bigc(a, v, sm, ph, buf(s), buf(s + 1), crank, C, ring, ring + 3 * (size_t)nv,
+      micro_phase_bigc<AD>(a, v, sm, ph, buf(s), buf(s + 1), crank, C, ring, ring + 3 * (size_t)nv,
                        mbar, bcnt);
     else
       micro_phase_big(a, v, sm, ph, buf(s), buf(s + 1), wg, nwg);
@@ -3609,6 +3611,56 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
           a.kps = kk;
           a.sg = cc;
         }
+    }
+  }
+  // Hardware clusters of a persistent kernel that are not all resident run in
+  // waves, each a whole launch long (GPC packing admits fewer clusters than
+  // CTA slots / C: e.g. 33 clusters of 4 at one CTA per SM).  When this grid
+  // would need more than one wave, take the size <= C with the least
+  // waves x rows per CTA from the measured residency (big rows chose above).
+  if (a.sg <= 1 && a.kps == 1 && autok && C > 1 && !a.bigc) {
+    static size_t w_smem = 0;
+    static int w_max[17];
+    if (w_smem != smem) {
+      for (int cc = 0; cc <= 16; ++cc) w_max[cc] = -1;
+      w_smem = smem;
+    }
+    auto max_active = [&](int cc) {
+      if (w_max[cc] < 0) {
+        if (cc > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t qc = {};
+        qc.gridDim = dim3(cc);
+        qc.blockDim = dim3(NT);
+        qc.dynamicSmemBytes = smem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = cc;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &qc) != cudaSuccess) {
+          cudaGetLastError();
+          n = 0;
+        }
+        w_max[cc] = n;
+      }
+      return w_max[cc];
+    };
+    const int n0 = max_active(C);
+    if (n0 > 0 && a.B > n0) {
+      long long best = (long long)((a.B + n0 - 1) / n0) * ((a.m.nx + C - 1) / C);
+      for (int cc = C - 1; cc >= 1; --cc) {
+        const int n = max_active(cc);
+        if (n <= 0) continue;
+        const long long cost = (long long)((a.B + n - 1) / n) * ((a.m.nx + cc - 1) / cc);
+        if (cost < best) {
+          best = cost;
+          C = cc;
+        }
+      }
+      if (dbg_packing) fprintf(stderr, "pk packing: B %d does not fit in one wave, clusters of %d\n", a.B, C);
     }
   }
   const bool sg = a.sg > 1;

@@ -55,7 +55,7 @@ def main(tag):
     tot = sum(v[1] for v in agg.values())
     with open(os.path.join(PROF, f"{tag}_launch_list.txt"), "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none --csv:\n"
-                "#   python bench.py --steps 2 --warmup 3 --no-cpu --no-parareal\n"
+                "#   python bench.py --steps 2 --warmup 3 --no-cpu --no-extras\n"
                 "# cold-cache, serialised per-launch times: compare SHARES (bench.py's CUDA events\n"
                 "# give the absolute numbers); field_kernel launches are input setup outside the\n"
                 "# timed region; fine launches = 3 warm-up + 2 timed + 2 pipeline warm-up + 2 e2e\n")
@@ -79,7 +79,7 @@ def main(tag):
                            capture_output=True, text=True).stdout
     with open(os.path.join(PROF, f"{tag}_fine_kernel_ncu.txt"), "w") as f:
         f.write("# ncu --set full --clock-control none --import-source on -k regex:fine_kernel -c 1\n"
-                "#   python bench.py --steps 1 --warmup 3 --no-cpu --no-parareal "
+                "#   python bench.py --steps 1 --warmup 3 --no-cpu --no-extras "
                 "(cfg5: 256 x 1024x128, 500 steps)\n")
         f.write(f"# kernel: {get('Kernel Name')}\n\n")
         for k in KEYS:
