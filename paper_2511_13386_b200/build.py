@@ -29,7 +29,7 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-FINE_PARTS = 8  # pk_fine.cu compiles once per PK_FINE_PART (one fine_kernel layout each)
+FINE_PARTS = 9  # pk_fine.cu compiles once per PK_FINE_PART (one fine_kernel layout each)
 
 
 def build(force: bool = False, verbose: bool = False, extra=(), jobs: int | None = None) -> str:

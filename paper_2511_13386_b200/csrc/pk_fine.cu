@@ -1056,7 +1056,7 @@ __device__ bool prepare_step_fused(const FineArgs& a, const SliceView& v, const 
         ++mine.cnt;
       }
     KSeg ex;
-    KSeg tot = kseg_block_scan(mine, ex, sm.misc + 8);  // (barrier: P4 is done here)
+    KSeg tot = kseg_block_scan(mine, ex, sm.misc + 64);  // (barrier: P4 is done here)
     if (P.dist) {  // CTA totals meet in the leader's reduction scratch (free here)
       int* ct = reinterpret_cast<int*>(cg::this_cluster().map_shared_rank(sm.red, 0)) + 576;
       if (threadIdx.x == 0) {
@@ -1742,6 +1742,19 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   const double k1u = P.k1s ? P.k1s[v.b] : NaN_, k2u = P.k2s ? P.k2s[v.b] : NaN_;
   const bool kuni = k1u == k1u && k2u == k2u;
   auto rowid = [&](int p) { return DENSE ? p : __ldcg(v.klist + p); };
+  // listed rows: this warp's next 32 row ids ride in the lanes (one L2 round
+  // trip for the producer logic and the first coefficient batch together; a
+  // load per listed row made the start of a sparse phase a chain of them)
+  int rw_base = p0;
+  int rw = (!DENSE && p0 + lane < p1) ? __ldcg(v.klist + p0 + lane) : 0;
+  auto rowid_u = [&](int p) {  // p uniform over the warp
+    if (DENSE) return p;
+    if (p - rw_base >= 32) {
+      rw_base = p;
+      rw = p + lane < p1 ? __ldcg(v.klist + p + lane) : 0;
+    }
+    return __shfl_sync(FULL, rw, p - rw_base);
+  };
 
   if (lane == 0) fence_proxy_async_global();  // rows written by the generic proxy, read by TMA
   __syncwarp();
@@ -1797,7 +1810,7 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
     while (st.q_prod < q_limit) {
       if (st.e_next > st.e_end) {
         if (st.p_prod >= p1) break;
-        const int i = rowid(st.p_prod++);
+        const int i = rowid_u(st.p_prod++);
         st.e_next = max(i - 1, st.hi_p + 1);
         st.e_end = i + 1;
         continue;
@@ -1840,7 +1853,7 @@ __device__ void micro_phase_g8(const FineArgs& a, const SliceView& v, const Smem
   auto load_batch = [&](int base, Coef& c) {
     const int pl = base + lane;
     if (pl < p1) {
-      const int r = rowid(pl);
+      const int r = (!DENSE && base == rw_base) ? rw : rowid(pl);
       // signed E-upwind factor: (g - g_nb) * (+-vco) reproduces both of the
       // reference's forms bitwise (kinetic.py:176-187); 0 when E == 0
       const int sg = __ldcg(v.vsg + r);
@@ -2060,6 +2073,15 @@ __device__ void micro_phase_pc(const FineArgs& a, const SliceView& v, int ph, co
     const int i0 = dense ? e0 : __ldcg(v.klist + e0);
     int pw = e0;
     int jw = 0;  // next operation whose completion has not been observed
+    // stream positions of the entries after pw, 32 at a time in the lanes
+    // (kpos is increasing): one L2 round trip per 32 entries -- walking kpos
+    // entry by entry cost a dependent L2 load per entry, ~700 cycles a row,
+    // and bounded the whole sparse micro phase
+    auto kwin = [&](int base) {
+      const int q = base + 1 + lane;
+      return !dense && q < e1 ? __ldcg(v.kpos + q) - kp0 : 0x7fffffff;
+    };
+    int wb = e0, kq = kwin(e0);
     for (int g = 0; g < ngrp; ++g) {
       const uint32_t G = (qbase >> 3) + (uint32_t)g;
       if (g >= NG) {
@@ -2071,8 +2093,16 @@ __device__ void micro_phase_pc(const FineArgs& a, const SliceView& v, int ph, co
         if (dense) {
           plast = min(e0 + x, e1 - 1);
         } else {
-          // position of row i-1 of entry p is kpos[p] - kpos[e0]
-          while (pw + 1 < e1 && __ldcg(v.kpos + pw + 1) - kp0 <= x) ++pw;
+          // position of row i-1 of entry p is kpos[p] - kpos[e0]: the last
+          // entry whose rows start at or before x
+          for (;;) {
+            const int off = pw - wb;  // lane off + t holds entry pw + 1 + t
+            const unsigned bal = __ballot_sync(FULL, lane >= off && kq <= x) >> off;
+            pw += bal == FULL ? 32 : __ffs(~bal) - 1;
+            if (pw - wb < 32) break;
+            wb = pw;  // window used up: the next 32 entries
+            kq = kwin(wb);
+          }
           plast = pw;
         }
         const int jl = (plast - e0) / RPO;
@@ -2850,8 +2880,8 @@ __device__ __forceinline__ void group_barrier(unsigned* cnt, int C, unsigned& n)
 // AD: adaptation on (hybrid) or off (all-kinetic, compiled without the
 // labels / lifts / row lists of the hybrid slice phase)
 template <int T, int S, int G, int NT, bool AD>
-// (the G8 layouts with 8 warps run one CTA per SM: the full register file)
-__global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128)) ? 1 : 2)
+// (the G8 layouts with 8 warps and the GS layout with 16 run one CTA per SM)
+__global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128) || (G < 0 && NT > 256)) ? 1 : 2)
     fine_kernel(const FineArgs a) {
   // ring row stride (doubles); G > 0: per-warp G8 rings, G < 0: CTA-wide
   // producer/consumer ring of the GS layout with SEG = -G
@@ -2910,7 +2940,7 @@ __global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128)) ? 1 : 2)
       sm.w2 = const_cast<double*>(m.w2);
     }
     sm.red = reinterpret_cast<double*>(p); p += 2 * (MAX_LEAF + MAX_NODE) * 8;
-    sm.misc = reinterpret_cast<int*>(p); p += 64 * 4;
+    sm.misc = reinterpret_cast<int*>(p); p += 160 * 4;
     sm.wrow = reinterpret_cast<double*>(p);
     if (T == 0) p += (size_t)nwpc * nv * 8;       // generic-layout row scratch
     if (T < 0 && !a.bigc) p += (size_t)nwpc * BIG_SCR * 8;   // big rows: plan scratch
@@ -3331,7 +3361,7 @@ constexpr int kThreads = 256;
 
 static size_t base_smem(int nv, int T, int S, int G, int NT) {
   size_t s = 128 * 8 + (sizeof(PwPlan) + 15) / 16 * 16 + (T >= 0 ? 4 * (size_t)nv * 8 : 0) +
-             2 * (MAX_LEAF + MAX_NODE) * 8 + 64 * 4;
+             2 * (MAX_LEAF + MAX_NODE) * 8 + 160 * 4;
   if (T < 0) s += (NT / 32) * (size_t)BIG_SCR * 8;
   else if (T == 0) s += (NT / 32) * (size_t)nv * 8;
   else if (G < 0) s += (size_t)S * (nv + 8) * 8;
@@ -3407,9 +3437,9 @@ static cudaError_t launch_TA(FineArgs a, int C, cudaStream_t st) {
   auto kern = fine_kernel<T, S, G, NT, AD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if constexpr (G > 0 && NT > 128) {
-    // the 8-warp G8 layout only when every cluster of the grid is resident
-    // at one CTA per SM; else the caller falls back to 4 warps
+  if constexpr ((G > 0 && NT > 128) || (G < 0 && NT > 256)) {
+    // the wide layouts (8-warp G8, 16-warp GS) only when every cluster of the
+    // grid is resident at one CTA per SM; else the caller falls back
     if ((size_t)a.B * C > (size_t)num_sms) return cudaErrorNotSupported;
     if (C > 1) {
       if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
@@ -3753,6 +3783,11 @@ static cudaError_t launch_T(const FineArgs& a, int C, cudaStream_t st) {
 #else
 #define PK_LAYOUT_BODY_7(name, ...)
 #endif
+#if PK_IN_PART(8)
+#define PK_LAYOUT_BODY_8(name, ...) PK_LAYOUT_DEF(name, __VA_ARGS__)
+#else
+#define PK_LAYOUT_BODY_8(name, ...)
+#endif
 PK_LAYOUT(0, fine_generic, 0, 1, 0, 256)      // generic rows (<= 256 nodes)
 PK_LAYOUT(1, fine_big, -1, 1, 0, 256)         // big 1D-3V rows
 PK_LAYOUT(2, fine_g8_64w, 2, 16, 4, 256)      // nv = 64, G8, 8 warps
@@ -3761,6 +3796,7 @@ PK_LAYOUT(4, fine_g8_128w, 4, 14, 8, 256)     // nv = 128, G8, 8 warps
 PK_LAYOUT(5, fine_g8_128, 4, 14, 8, 128)      // nv = 128, G8, 4 warps
 PK_LAYOUT(6, fine_gs_256, 8, 20, -4, 256)     // nv = 256, producer/consumer
 PK_LAYOUT(7, fine_tma_512, 16, 3, 0, 256)     // nv = 512
+PK_LAYOUT(8, fine_gs_256w, 8, 40, -4, 512)    // nv = 256, 15 consumer warps, 40-row ring
 
 #if PK_IN_PART(0)
 template <int T>
@@ -3930,7 +3966,13 @@ cudaError_t launch_fine(const FineArgs& a, int C, cudaStream_t st) {
       return e;
       // (8 warps at two CTAs per SM, <= 128 registers: no spills, but the micro
       // loop loses its ILP and the step takes 1.6x longer)
-    case 256: return fine_gs_256(a, C, st);
+    case 256:
+      // few slices at one CTA per SM (cfg4's 8 windows per GPU: kinetic rows
+      // are served one per consumer warp at ~4k cycles each): 15 consumer
+      // warps and a 40-row ring instead of 7 and 20
+      if (wide) e = fine_gs_256w(a, C, st);
+      if (e == cudaErrorNotSupported) e = fine_gs_256(a, C, st);
+      return e;
     case 512: return fine_tma_512(a, C, st);
     default:
       if (a.m.nv <= 32 * GT) return fine_generic(a, C, st);

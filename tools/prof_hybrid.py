@@ -87,6 +87,9 @@ def main():
         ncta = min(a.B * Cc, 1024)
         smid = [int(x) for x in cc[34:34 + 3 * ncta:3]]
         shared = len(smid) - len(set(smid))
+        pm = [int(x) // ns for x in cc[32:32 + 3 * Cc:3]]
+        pb = [int(x) // ns for x in cc[33:33 + 3 * Cc:3]]
+        print(f"   slice 0 per-CTA cycles/step: micro {pm}, barrier after it {pb}")
         print(f"   clusters of {Cc}: {ncta} CTAs on {len(set(smid))} SMs ({shared} CTAs share an SM); "
               f"slice 0's CTAs on SMs {smid[:Cc]}")
 
