@@ -2139,6 +2139,10 @@ __device__ void micro_phase_pc(const FineArgs& a, const SliceView& v, int ph, co
     int c_row = 0, c_pos = 0;
     int jb = -1 << 30;  // first operation of the loaded batch
     constexpr int OPB = 32 / RPO;
+    // optional profile (slice 0's leader CTA, consumer warp 0): cycles spent
+    // on coefficients, waiting for rows, and in the row operation
+    const bool cprof = a.prof && v.b == 0 && warp == 0 && blockIdx.x == 0;
+    long long tq0 = cprof ? clock64() : 0, tq_coef = 0, tq_wait = 0, tq_op = 0;
     for (int j = warp; j < nops; j += nc) {
       const int jj = (j - warp) / nc;  // this warp's operation ordinal
       if (jj - jb >= OPB) {
@@ -2172,6 +2176,7 @@ __device__ void micro_phase_pc(const FineArgs& a, const SliceView& v, int ph, co
       const bool up = rsg >= 0;
       const int i = up ? rsg : -1 - rsg;
       double f[4], h[4];
+      if (cprof) { const long long t = clock64(); tq_coef += t - tq0; tq0 = t; }
       if (active) {
         uint32_t ra[3];
 #pragma unroll
@@ -2180,6 +2185,7 @@ __device__ void micro_phase_pc(const FineArgs& a, const SliceView& v, int ph, co
           mbar_wait_u32(s_full + 8 * (G % NG), (G / NG) & 1);
           ra[d] = s_ring + ((G % NG) * 8 + (Qp & 7)) * (RS * 8);
         }
+        if (cprof) { const long long t = clock64(); tq_wait += t - tq0; tq0 = t; }
         const uint32_t rp = ra[0], rc = ra[1], rn = ra[2];
         double* row = gout + (size_t)i * NV;
 #pragma unroll
@@ -2247,6 +2253,12 @@ __device__ void micro_phase_pc(const FineArgs& a, const SliceView& v, int ph, co
         v.fl_w[i] = bx * dv3;
         v.sq_w[i] = bq * dv3;
       }
+      if (cprof) { const long long t = clock64(); tq_op += t - tq0; tq0 = t; }
+    }
+    if (cprof && lane == 0) {
+      a.prof[29] += tq_coef;
+      a.prof[30] += tq_wait;
+      a.prof[31] += tq_op;
     }
   }
   qbase += (uint32_t)(8 * ngrp);

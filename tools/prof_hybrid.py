@@ -83,6 +83,8 @@ def main():
               "zero %d, klist %d, kstream %d" % tuple(int(x) // ns for x in cc[16:25]))
         print("   rows/step: flipped %.1f, zeroed %.1f, kinetic %.1f"
               % tuple(float(x) / ns for x in cc[26:29]))
+        print("   GS consumer warp 0 cycles/step: coefficients %d, waiting for rows %d, row operations %d"
+              % tuple(int(x) // ns for x in cc[29:32]))
         Cc = dev.last_launch()[0]
         ncta = min(a.B * Cc, 1024)
         smid = [int(x) for x in cc[34:34 + 3 * ncta:3]]
