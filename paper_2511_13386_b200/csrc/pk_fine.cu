@@ -507,8 +507,16 @@ static __device__ bool slice_field(const MeshDev& m, const double* rho, double r
     // (chunk by chunk, the carry continuing the chain, when nx > scan_cap)
     double defect, abssum;
     PK_TICK(0)
-    block_pairwise2([&](int i) { return (rho[i] - rb) * m.dx; }, [&](int i) { return fabs(rho[i]); },
-                    *sm.plan, sm.red, defect, abssum);
+    if (sm.plan->perfect) {  // (butterfly tree, 16 operands in flight per lane: pw_perfect)
+      double r2[2];
+      pw_perfect<2>([&](int s, int i) { return s ? fabs(rho[i]) : (rho[i] - rb) * m.dx; }, *sm.plan,
+                    sm.red, r2);
+      defect = r2[0];
+      abssum = r2[1];
+    } else {
+      block_pairwise2([&](int i) { return (rho[i] - rb) * m.dx; },
+                      [&](int i) { return fabs(rho[i]); }, *sm.plan, sm.red, defect, abssum);
+    }
     PK_TICK(1)
     if (fabs(defect) > rtol * fmax(abssum * m.dx, 2.2250738585072014e-308)) return false;
     const double corr = defect / (double)nx;
@@ -520,8 +528,15 @@ static __device__ bool slice_field(const MeshDev& m, const double* rho, double r
       smem_cumsum_call(sc, sc, nx, -0.0);
       __syncthreads();
       PK_TICK(3)
-      const double mean =
-          block_pairwise([&](int i) { return sc[i]; }, *sm.plan, sm.red) / (double)nx;
+      double mean;
+      if (sm.plan->perfect) {
+        const uint32_t scs = (uint32_t)__cvta_generic_to_shared(sc);
+        double mm[1];
+        pw_perfect<1>([&](int, int i) { return lds64(scs + 8 * i); }, *sm.plan, sm.red, mm);
+        mean = mm[0] / (double)nx;
+      } else {
+        mean = block_pairwise([&](int i) { return sc[i]; }, *sm.plan, sm.red) / (double)nx;
+      }
       PK_TICK(4)
       for (int i = threadIdx.x; i < nx; i += blockDim.x) E_out[i] = sc[i] - mean;
       __syncthreads();
