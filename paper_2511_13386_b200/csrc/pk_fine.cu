@@ -578,9 +578,9 @@ static __device__ bool slice_field(const MeshDev& m, const double* rho, double r
     double mean;
     const uint32_t rs = (uint32_t)__cvta_generic_to_shared(rho);  // on chip: shared memory
     if (!field_exact_onchip([&](int i) { return fabs(lds64(rs + 8 * i)); }, E_out, nx, m.dx, rtol,
-                            *sm.plan, sm.red, mean))
+                            *sm.plan, sm.red, mean, dbg ? dbg + 1 : nullptr))
       return false;
-    PK_TICK(3)
+    if (dbg) c0 = clock64();  // (field_exact_onchip ticked pairwise2 / corr / cumsum / mean)
     if (mean_out) {  // the caller applies E - mean where it next reads E
       *mean_out = mean;
     } else {
