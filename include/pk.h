@@ -135,6 +135,16 @@ int32_t pk_fine_last_launch(pk_ctx* ctx, int32_t out[4]);
  * rho, E_prev, kc, ki are read and written; E is written (the field after
  * the last step); g_a holds g on entry and on exit (g_b is scratch of the
  * same size). */
+/* Ask the fine launch in flight on `ctx` to stop: its slices return at their
+ * next step without writing results (the status record stays as it is).
+ * Stream-ordered on `stream`, which must NOT be the stream of that launch
+ * (it is busy with it); the request is cleared, in stream order, by the next
+ * pk_fine_propagate on this context.  For speculative work that is no longer
+ * needed (the overlapped parareal schedule starts the next iteration's windows
+ * before convergence is known; the reference has no counterpart).  Slices run
+ * as one hardware cluster each honour it; packed ensembles ignore it. */
+int32_t pk_fine_cancel(pk_ctx* ctx, void* stream);
+
 int32_t pk_fine_propagate(pk_ctx* ctx, int32_t B,
                           double* rho, double* E, double* E_prev,
                           uint8_t* kc, uint8_t* ki,

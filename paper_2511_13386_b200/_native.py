@@ -69,6 +69,7 @@ SIGNATURES = {
     "pk_status_read": (C.c_int32, [C.c_void_p, C.POINTER(PkStatus), C.c_int32]),
     "pk_status_read_stream": (C.c_int32, [C.c_void_p, C.POINTER(PkStatus), C.c_int32, C.c_void_p]),
     "pk_fine_last_launch": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "pk_fine_cancel": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "pk_fine_propagate": (C.c_int32, [
         C.c_void_p, C.c_int32,
         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -37,6 +37,7 @@ struct pk_ctx {
   double* d_const = nullptr;  // vx | M | xiM | w2
   PwPlan* d_plan = nullptr;  // [x: nx terms, folded velocity row, middle xi plane]
   pk::Status* d_status = nullptr;
+  int* d_cancel = nullptr;  // cancel request of the fine launch in flight (pk_fine_cancel)
   int cap = 0;
   // workspace
   double* dws = nullptr;  // 16 double arrays of cap*nx
@@ -278,7 +279,8 @@ pk_ctx* pk_create(int32_t device, const pk_mesh* mesh) {
   }
   if (cudaMalloc(&c->d_const, h.size() * 8) != cudaSuccess ||
       cudaMalloc(&c->d_plan, 3 * sizeof(PwPlan)) != cudaSuccess ||
-      cudaMalloc(&c->d_status, sizeof(pk::Status)) != cudaSuccess) {
+      cudaMalloc(&c->d_status, sizeof(pk::Status)) != cudaSuccess ||
+      cudaMalloc(&c->d_cancel, sizeof(int)) != cudaSuccess) {
     delete c;
     return nullptr;
   }
@@ -302,6 +304,7 @@ void pk_destroy(pk_ctx* c) {
   cudaFree(c->d_const);
   cudaFree(c->d_plan);
   cudaFree(c->d_status);
+  cudaFree(c->d_cancel);
   delete c;
 }
 
@@ -407,6 +410,10 @@ int32_t pk_fine_propagate(pk_ctx* c, int32_t B, double* rho, double* E, double* 
   a.eps2 = hyb->eps2;
   a.rtol = field_rtol;
   bind_ws(c, a);
+  // a cancel request is for the launch in flight: cleared in stream order
+  a.cancel = c->d_cancel;
+  if (cudaMemsetAsync(c->d_cancel, 0, sizeof(int), S(stream)) != cudaSuccess)
+    return cuda_fail(c, cudaGetLastError(), "cancel flag");
   // cluster size: enough CTAs to fill the chip, >= 4 rows per warp
   int C = cluster_hint;
   if (C <= 0) {
@@ -532,6 +539,16 @@ int32_t pk_jump(pk_ctx* c, int64_t n, const double* a, const double* b, double* 
   cudaSetDevice(c->device);
   cudaError_t e = pk::launch_jump(n, a, b, out, c->d_status, S(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "jump launch");
+  return PK_OK;
+}
+
+int32_t pk_fine_cancel(pk_ctx* c, void* stream) {
+  if (!c) return PK_ERR_BAD_ARG;
+  cudaSetDevice(c->device);
+  // (bytes 0x01: a non-zero int) in the order of `stream` -- NOT the stream of
+  // the launch to cancel, which is busy with it
+  if (cudaMemsetAsync(c->d_cancel, 1, sizeof(int), S(stream)) != cudaSuccess)
+    return cuda_fail(c, cudaGetLastError(), "pk_fine_cancel");
   return PK_OK;
 }
 

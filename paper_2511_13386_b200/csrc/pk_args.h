@@ -53,6 +53,7 @@ struct FineArgs {
                          // cluster; moments through global memory, barriers on sg_cnt)
   unsigned* sg_cnt;      // [B] per-group arrival counters (zeroed by the launcher)
   int bigc;              // big rows, one CTA per row through shared-memory row buffers (launcher)
+  const int* cancel;     // host cancel request (pk_fine_cancel): the slice owners abort at the next step
   int pass_prepare;      // hybrid slice phase of one CTA: the pass-by-pass form instead of
                          // prepare_step_cta (A/B switch PK_PASS_PREPARE=1)
   // state

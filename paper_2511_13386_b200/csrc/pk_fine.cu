@@ -3233,6 +3233,11 @@ __global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128) || (G < 0 &&
       if (!ok && threadIdx.x == 0) *abort_flag = 1;
       if (prof) { c1 = clock64(); tp[3] += c1 - c0; c0 = c1; }
     }
+    // host cancel request (speculative parareal windows that are not needed
+    // any more): sampled by the slice's leader thread only and passed on as an
+    // abort before the barrier, so every CTA of the cluster sees the same value
+    if (K == 1 && a.sg <= 1 && leader && threadIdx.x == 0 && a.cancel && __ldcg(a.cancel))
+      *abort_flag = 1;
     barrier();
     if (prof) { c1 = clock64(); tp[4] += c1 - c0; c0 = c1; }
     if (K == 1 && __ldcg(abort_flag)) return;

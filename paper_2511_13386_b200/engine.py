@@ -290,6 +290,11 @@ class Device:
             msg = self.lib.pk_last_error(self.ctx)
             raise_for(code, f"{what}: {msg.decode() if msg else ''}")
 
+    def cancel(self, stream):
+        """Ask the fine launch in flight on this context to stop (pk_fine_cancel);
+        `stream`: a torch stream other than the launch's own."""
+        self._rc(self.lib.pk_fine_cancel(self.ctx, C.c_void_p(stream.cuda_stream)), "pk_fine_cancel")
+
     def last_launch(self):
         """Layout of this thread's last fine launch: (CTAs per cluster or group,
         slices per cluster, slice vectors in shared memory, kind: 0 hardware

@@ -541,6 +541,7 @@ class _Overlap:
         # correction (the critical path) takes a high-priority stream of its
         # own; each window one low-priority stream for both parities
         self.cs = torch.cuda.Stream(dv, priority=-1)
+        self.side = None  # cancel requests (sync)
         ws = [torch.cuda.Stream(dv) for _ in range(ng)]
         self.fs = [None] + [[s, s] for s in ws]
         f64 = dict(dtype=torch.float64, device=dv)
@@ -739,6 +740,18 @@ class _Overlap:
         self.D.zero_()
 
     def sync(self):
+        """Wait for the work in flight.  Fine windows enqueued speculatively for
+        an iteration that will not happen (the run converged, hit k_max or
+        failed) are asked to stop first: they would run their whole window
+        (cfg2: ~8 ms of a ~50 ms run) only to be dropped."""
+        if self.spec is not None:
+            torch = self.torch
+            if self.side is None:
+                self.side = torch.cuda.Stream(self.cs.device)
+            for pair in self.devs[1:]:
+                for d in pair:
+                    d.cancel(self.side)
+            self.side.synchronize()
         for pair in self.fs[1:]:
             pair[0].synchronize()
         self.cs.synchronize()

@@ -60,3 +60,52 @@ def test_hybrid_clusters_fit_one_wave():
     two = _hybrid_batch(nx, nv, 5, steps, hint=2)
     for a, b in zip(two[:4], one[:4]):
         assert np.array_equal(a[0], b[0])
+
+
+def test_fine_cancel_stops_a_window():
+    """pk_fine_cancel: a window launched for far more steps than needed (the
+    overlapped parareal schedule's speculative windows) stops at its next step
+    when asked, and the context runs the next launch normally."""
+    import time
+
+    import torch
+
+    import paper_2511_13386_b200 as pk
+    from paper_2511_13386_b200.engine import Device, make_phase
+
+    nx, nv = 256, 64
+    m = pk.build_mesh(pk.MeshSpec(nx=nx, nvx=nv))
+    rho = 1.0 + 0.3 * np.cos(m.x_centers)
+    rb = float(rho.sum() * m.dx / m.x_star)
+    E0 = pk.solve_field(rho, rb, m)
+    eps = 1e-2
+    p = pk.KineticStepParams.default(m, eps, e_max=float(np.abs(E0).max()))
+    dev = Device.for_mesh(m)
+    knobs = pk.hybrid.knobs_of(pk.HybridOptions(adaptation=False), pk.Thresholds(1e-3, 1e-3))
+
+    def launch(steps):
+        phases = [make_phase(m, [eps], [p.dt], [steps]), make_phase(m, [eps], [p.dt], [0])]
+        r = dev.t(rho[None].copy())
+        E = dev.t(E0[None].copy())
+        Ep = E.clone()
+        kc = dev.t(np.ones((1, nx), dtype=np.uint8))
+        ki = kc.clone()
+        g = dev.t(np.zeros((1, nx, nv)))
+        dev.fine(r, E, Ep, kc, ki, g, dev.t(np.full(1, rb)), [3], phases, knobs, [eps], 1e-5)
+        return r, g
+
+    ref_r, ref_g = launch(50)
+    dev.check()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    t0 = time.perf_counter()
+    launch(200000)               # ~1.5 s of steps if left alone
+    time.sleep(0.02)
+    dev.cancel(side)
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t0 < 0.5
+    dev.check()                  # a cancelled launch latches no error
+    r, g = launch(50)            # the request was for that launch only
+    dev.check()
+    assert np.array_equal(r.cpu().numpy(), ref_r.cpu().numpy())
+    assert np.array_equal(g.cpu().numpy(), ref_g.cpu().numpy())
