@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -411,7 +412,8 @@ int32_t pk_fine_propagate(pk_ctx* c, int32_t B, double* rho, double* E, double* 
   a.rtol = field_rtol;
   bind_ws(c, a);
   // a cancel request is for the launch in flight: cleared in stream order
-  a.cancel = c->d_cancel;
+  static const bool no_cancel = getenv("PK_NO_CANCEL") != nullptr;  // (A/B switch)
+  a.cancel = no_cancel ? nullptr : c->d_cancel;
   if (cudaMemsetAsync(c->d_cancel, 0, sizeof(int), S(stream)) != cudaSuccess)
     return cuda_fail(c, cudaGetLastError(), "cancel flag");
   // cluster size: enough CTAs to fill the chip, >= 4 rows per warp

@@ -3209,6 +3209,12 @@ __global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128) || (G < 0 &&
     }
     if (prof) { c1 = clock64(); tp[1] += c1 - c0; c0 = c1; }
     if (profc) pc_b += clock64() - pc_t;
+    // host cancel request (speculative parareal windows that are not needed
+    // any more): sampled by the slice's leader thread only, here, so that the
+    // load's L2 round trip hides behind the slice phase
+    int cancel_req = 0;
+    if (K == 1 && a.sg <= 1 && leader && threadIdx.x == 0 && a.cancel)
+      asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(cancel_req) : "l"(a.cancel));
     // (K == 1: s < nst always, and an aborted slice has returned)
     if ((dist || leader) && s < nst && !(K > 1 && __ldcg(abort_flag))) {
       bool ok = finish_step(a, v, sm, ph, s, par);
@@ -3233,11 +3239,9 @@ __global__ void __launch_bounds__(NT, (T < 0 || (G > 0 && NT > 128) || (G < 0 &&
       if (!ok && threadIdx.x == 0) *abort_flag = 1;
       if (prof) { c1 = clock64(); tp[3] += c1 - c0; c0 = c1; }
     }
-    // host cancel request (speculative parareal windows that are not needed
-    // any more): sampled by the slice's leader thread only and passed on as an
-    // abort before the barrier, so every CTA of the cluster sees the same value
-    if (K == 1 && a.sg <= 1 && leader && threadIdx.x == 0 && a.cancel && __ldcg(a.cancel))
-      *abort_flag = 1;
+    // (the cancel request sampled above, passed on as an abort before the
+    // barrier, so every CTA of the cluster sees the same value)
+    if (cancel_req) *abort_flag = 1;
     barrier();
     if (prof) { c1 = clock64(); tp[4] += c1 - c0; c0 = c1; }
     if (K == 1 && __ldcg(abort_flag)) return;
