@@ -2868,6 +2868,14 @@ __device__ __forceinline__ void cluster_barrier(int C) {
   if (C > 1) {
     cg::this_cluster().sync();
   } else {
+    // one CTA per slice: the next micro phase's bulk copies (async proxy, from
+    // L2) read rows that OTHER warps of this CTA stored in this phase.
+    // __syncthreads() orders them for the CTA's threads only; the stores
+    // must also be performed at L2 before the copies are issued (the cluster
+    // and group barriers release at cluster / gpu scope and imply it).
+    // Without the fence a slice now and then read a stale halo row
+    // (tools/flake_probe.py: 3 of 24 fresh processes, last-bit differences).
+    __threadfence();
     __syncthreads();
   }
 }

@@ -62,6 +62,7 @@ def test_hybrid_clusters_fit_one_wave():
         assert np.array_equal(a[0], b[0])
 
 
+@pytest.mark.skipif("PK_NO_CANCEL" in __import__("os").environ, reason="A/B switch: cancel disabled")
 def test_fine_cancel_stops_a_window():
     """pk_fine_cancel: a window launched for far more steps than needed (the
     overlapped parareal schedule's speculative windows) stops at its next step
