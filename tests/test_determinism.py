@@ -70,7 +70,8 @@ def _ensemble_run(nx, nv, B, steps, hint=0):
 @pytest.mark.parametrize("nx,nv,B,hint,kind", [(256, 128, 256, 0, 1),   # software groups
                                                (128, 64, 200, 0, 0),    # packed clusters
                                                (512, 128, 16, 0, 0),    # one slice per cluster
-                                               (64, 256, 40, 0, None)])  # nv = 256 layout
+                                               (64, 256, 40, 0, None),   # nv = 256 layout
+                                               (256, 128, 256, 1, 0)])   # one CTA per slice
 def test_layouts_repeat_bitwise(nx, nv, B, hint, kind):
     outs = _ensemble_run(nx, nv, B, 12, hint)
     if kind is not None and "PK_NO_SG" not in os.environ:
