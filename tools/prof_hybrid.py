@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--rtol", type=float, default=1e-5)
     ap.add_argument("--fast", action="store_true", help="fast scan mode (pk.scan_mode(False))")
+    ap.add_argument("--hint", type=int, default=0, help="cluster size (0: the launcher's choice)")
     a = ap.parse_args()
     import torch
 
@@ -60,7 +61,7 @@ def main():
         e0.record(torch.cuda.current_stream())
         # bit0: lift g from (rho, E) at entry; bit1: E_prev := E (a window restart)
         dev.fine(rho, E, Ep, kc, ki, g, rb, [3] * a.B, phases, knobs, [c.eps] * a.B, a.rtol,
-                 prepared=prepared)
+                 prepared=prepared, cluster_hint=a.hint)
         e1.record(torch.cuda.current_stream())
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
